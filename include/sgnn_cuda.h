@@ -1,0 +1,249 @@
+/*
+ * sgnn_cuda.h -- C-ABI of the B200-native (sm_100a) GCN/GAT layer library
+ * (libsgnn_cuda.so).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * This is the drop-in boundary for the reference `sgnn` layer API
+ * (/root/reference/proj/include/sgnn/): every entry point names the reference
+ * interface it replaces.  The reference binds its C++ API to Python through
+ * pybind11 (python/bindings.cpp); the binding a maintainer would add over this
+ * ABI (ctypes) is shown in INTEGRATION.md and implemented in
+ * paper_2308_12093_b200/_capi.py.
+ *
+ * Conventions
+ *  - Device pointers unless a parameter says "host".  All work is enqueued on
+ *    the stream of the sgnn_ctx; calls that return a size through a host
+ *    pointer synchronize that stream.
+ *  - Indices int32 (ref common.hpp:16), counts int64 (common.hpp:17).
+ *  - Dense matrices row-major.  Multi-head operands are n x (h*k) slabs with
+ *    the head in the middle (ref gat.hpp:19-20).  Per-edge per-head values on
+ *    the device are EDGE-major (q x h); the reference stores them head-major
+ *    (h x q, pattern.hpp:99-123) -- sgnn_gat_cache_edge_values converts.
+ *  - Errors: int status; SGNN_EINVAL where the reference throws
+ *    std::invalid_argument (common.hpp:37-43) with the same message text,
+ *    retrievable through sgnn_last_error() (thread-local).
+ */
+#ifndef SGNN_CUDA_H
+#define SGNN_CUDA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGNN_OK 0
+#define SGNN_EINVAL 1   /* std::invalid_argument in the reference */
+#define SGNN_ERUNTIME 2 /* std::runtime_error in the reference      */
+#define SGNN_ECUDA 3
+#define SGNN_ENCCL 4
+
+typedef enum { SGNN_F32 = 0, SGNN_F64 = 1 } sgnn_dtype;
+
+/* sparse.hpp:22 SparseFormat */
+typedef enum {
+  SGNN_COO = 0,
+  SGNN_CSR = 1,
+  SGNN_CSC = 2,
+  SGNN_ELLPACK = 3,
+  SGNN_HYBRID = 4
+} sgnn_format;
+
+/* cost.hpp:114-122 GcnForward / GcnBackward / SchemeChoice */
+typedef enum {
+  SGNN_TRANSFORM_FIRST = 0,
+  SGNN_PROPAGATE_FIRST = 1,
+  SGNN_PROPAGATE_FIRST_CACHED = 2
+} sgnn_gcn_forward_scheme;
+typedef enum {
+  SGNN_FUSED_PROPAGATE = 0,
+  SGNN_SPLIT_PROPAGATE = 1,
+  SGNN_SPLIT_PROPAGATE_CACHED = 2
+} sgnn_gcn_backward_scheme;
+typedef struct {
+  int32_t forward;  /* sgnn_gcn_forward_scheme  */
+  int32_t backward; /* sgnn_gcn_backward_scheme */
+  int32_t caching;  /* bool */
+} sgnn_scheme;
+
+/* gcn.hpp:23 SchemePolicy */
+typedef enum {
+  SGNN_POLICY_ADAPTIVE = 0,
+  SGNN_POLICY_TRANSFORM_FIRST = 1,
+  SGNN_POLICY_PROPAGATE_FIRST = 2
+} sgnn_policy;
+
+/* cost.hpp:229 GatCacheLevel */
+typedef enum {
+  SGNN_GAT_NONE = 0,
+  SGNN_GAT_FEATURES = 1,
+  SGNN_GAT_NODE_ATTENTION = 2,
+  SGNN_GAT_FULL = 3
+} sgnn_gat_level;
+
+typedef struct sgnn_ctx_s* sgnn_ctx;
+typedef struct sgnn_adj_s* sgnn_adj;
+typedef struct sgnn_pattern_s* sgnn_pattern;
+typedef struct sgnn_gcn_cache_s* sgnn_gcn_cache;
+typedef struct sgnn_gat_cache_s* sgnn_gat_cache;
+
+/* ---- errors / context ------------------------------------------------ */
+/* common.hpp:37-43 require() message of the last failing call on this thread */
+const char* sgnn_last_error(void);
+const char* sgnn_version(void);
+/* stream: a cudaStream_t (NULL = create an owned non-blocking stream) */
+int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out);
+int sgnn_ctx_destroy(sgnn_ctx ctx);
+int sgnn_ctx_set_stream(sgnn_ctx ctx, void* stream);
+int sgnn_ctx_synchronize(sgnn_ctx ctx);
+/* number of kernels this context has launched (bench gpu_launches) */
+int sgnn_ctx_launch_count(sgnn_ctx ctx, int64_t* out);
+
+/* ---- host-pure: selector and analytic model (cost.hpp, gcn.hpp) --------- */
+/* cost.hpp:201-223 gcn_select_scheme */
+int sgnn_gcn_select_scheme(int64_t m, int64_t k, int needs_feature_grad, int caching,
+                           sgnn_scheme* out);
+/* gcn.hpp:34-47 resolve_scheme */
+int sgnn_resolve_scheme(int policy, int64_t m, int64_t k, int needs_feature_grad, int caching,
+                        sgnn_scheme* out);
+/* cost.hpp:143-197 */
+int64_t sgnn_gcn_forward_flops(int fwd, int64_t n, int64_t m, int64_t k, int64_t q);
+int64_t sgnn_gcn_backward_flops(int bwd, int64_t n, int64_t m, int64_t k, int64_t q, int fg);
+int64_t sgnn_gcn_forward_transients(int fwd, int64_t n, int64_t m, int64_t k);
+int64_t sgnn_gcn_backward_transients(int bwd, int64_t n, int64_t m, int64_t k, int fg);
+/* cost.hpp:63-101 spmm_cost / sddmm_cost */
+int sgnn_spmm_cost(int format, int64_t n, int64_t q, int64_t p, int64_t f, int64_t scalar_bytes,
+                   int64_t index_bytes, int64_t* flops, int64_t* bytes, double* oi);
+int sgnn_sddmm_cost(int format, int64_t n, int64_t q, int64_t p, int64_t f,
+                    int64_t scalar_bytes, int64_t index_bytes, int64_t* flops, int64_t* bytes,
+                    double* oi);
+/* cost.hpp:243-252 gat_cache_footprint */
+int64_t sgnn_gat_cache_footprint(int level, int64_t n, int64_t h, int64_t k, int64_t q,
+                                 int64_t scalar_bytes);
+
+/* ---- deterministic inputs (graph.hpp, dense.hpp, gcn.hpp, gat.hpp) ------- */
+/* graph.hpp:160-190 synthetic_graph; host buffers of sgnn_synthetic_graph_edges() */
+int64_t sgnn_synthetic_graph_edges(int32_t n, double avg_degree);
+int sgnn_synthetic_graph(int32_t n, double avg_degree, uint64_t seed, int32_t* host_src,
+                         int32_t* host_dst);
+/* dense.hpp:45-53 DenseMatrix::random_uniform, generated ON DEVICE: the
+ * splitmix64 stream is counter-based, draw i = mix(seed + (i+2)*golden) */
+int sgnn_random_uniform(sgnn_ctx ctx, int64_t rows, int64_t cols, uint64_t seed, double lo,
+                        double hi, int dtype, void* out);
+/* gcn.hpp:54-62 GcnParams::init (device outputs theta m x k, bias k) */
+int sgnn_gcn_params_init(sgnn_ctx ctx, int32_t m, int32_t k, uint64_t seed, int dtype,
+                         void* theta, void* bias);
+/* gat.hpp:36-52 GatParams::init */
+int sgnn_gat_params_init(sgnn_ctx ctx, int32_t m, int32_t h, int32_t k, uint64_t seed,
+                         int dtype, void* theta, void* a_src, void* a_dst, void* bias);
+
+/* ---- sparse-format layer, on device (sparse.hpp, pattern.hpp) ------------ */
+/* sparse.hpp:110-142 coo_from_triplets: range check, stable sort by (row,col),
+ * duplicates keep the LAST value.  Outputs have capacity nnz. */
+int sgnn_coo_canonicalize(sgnn_ctx ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                          const int32_t* rows, const int32_t* cols, const void* vals, int dtype,
+                          int32_t* out_rows, int32_t* out_cols, void* out_vals,
+                          int64_t* host_out_nnz);
+/* sparse.hpp:151-171 coo_to_csr (input canonical) */
+int sgnn_csr_from_coo(sgnn_ctx ctx, int32_t n_rows, int64_t nnz, const int32_t* rows,
+                      int32_t* rowptr);
+/* sparse.hpp:195-218 coo_to_csc; perm[p] = canonical index of CSC entry p
+ * (pattern.hpp:35-44).  out_vals/perm may be NULL. */
+int sgnn_csc_from_coo(sgnn_ctx ctx, int32_t n_cols, int64_t nnz, const int32_t* rows,
+                      const int32_t* cols, const void* vals, int dtype, int32_t* colptr,
+                      int32_t* out_rows, void* out_vals, int32_t* perm);
+/* sparse.hpp:457-472 add_self_loops (input canonical; capacity nnz + n) */
+int sgnn_add_self_loops(sgnn_ctx ctx, int32_t n, int64_t nnz, const int32_t* rows,
+                        const int32_t* cols, const void* vals, int dtype, int32_t* out_rows,
+                        int32_t* out_cols, void* out_vals, int64_t* host_out_nnz);
+/* sparse.hpp:474-495 gcn_normalize (input canonical; capacity nnz + n);
+ * degrees in float64 in canonical order, bit-identical to the reference */
+int sgnn_gcn_normalize(sgnn_ctx ctx, int32_t n, int64_t nnz, const int32_t* rows,
+                       const int32_t* cols, const void* vals, int dtype, int32_t* out_rows,
+                       int32_t* out_cols, void* out_vals, int64_t* host_out_nnz);
+
+/* kernels.hpp:191-211 AdjacencyOp: canonical COO -> device CSR (forward) and
+ * CSC (= CSR of A^T, the zero-copy transpose of sparse.hpp:400-420).  Any
+ * `format` is accepted: every reference format accumulates each output row
+ * in ascending column order, so results are identical. */
+int sgnn_adj_create(sgnn_ctx ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                    const int32_t* rows, const int32_t* cols, const void* vals, int dtype,
+                    int format, sgnn_adj* out);
+int sgnn_adj_destroy(sgnn_adj adj);
+int sgnn_adj_info(sgnn_adj adj, int32_t* n_rows, int32_t* n_cols, int64_t* nnz, int* dtype);
+/* device arrays of the operator (borrowed; valid while adj lives) */
+int sgnn_adj_arrays(sgnn_adj adj, const int32_t** rowptr, const int32_t** cols,
+                    const void** vals, const int32_t** colptr, const int32_t** crows,
+                    const void** cvals);
+
+/* pattern.hpp:19-59 SparsePattern::build from a device CSR */
+int sgnn_pattern_create(sgnn_ctx ctx, int32_t n, int64_t nnz, const int32_t* rowptr,
+                        const int32_t* cols, sgnn_pattern* out);
+int sgnn_pattern_destroy(sgnn_pattern p);
+int sgnn_pattern_info(sgnn_pattern p, int32_t* n, int64_t* nnz, int* all_self_loops);
+int sgnn_pattern_arrays(sgnn_pattern p, const int32_t** rowptr, const int32_t** cols,
+                        const int32_t** colptr, const int32_t** rows, const int32_t** perm,
+                        const int32_t** diag);
+
+/* ---- kernels (kernels.hpp, dense.hpp) ----------------------------------- */
+/* kernels.hpp:167-186 spmm / AdjacencyOp::multiply[_transposed]:
+ * C (n_rows x f) = A B (+ 1 bias^T if bias != NULL) */
+int sgnn_spmm(sgnn_ctx ctx, sgnn_adj adj, int transposed, const void* B, int32_t f, void* C,
+              const void* bias);
+/* kernels.hpp:301-337 sddmm (one head, no scale): out_e = B[i,:] . C[:,j];
+ * B n x f, C f x ldc */
+int sgnn_sddmm(sgnn_ctx ctx, sgnn_pattern p, const void* B, int32_t f, const void* C,
+               int32_t ldc, int dtype, void* out);
+/* kernels.hpp:500-534 edge_softmax, edge-major w/alpha (q x heads) */
+int sgnn_edge_softmax(sgnn_ctx ctx, sgnn_pattern p, int32_t heads, const void* w, int dtype,
+                      void* alpha);
+/* dense.hpp:97-157 gemm: C = op(A) op(B); A is ra x ca, B is rb x cb */
+int sgnn_gemm(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+              int32_t rb, int32_t cb, int trans_a, int trans_b, void* C);
+/* dense.hpp:272-282 column_sums: out (cols) = sum over rows */
+int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
+                     void* out);
+
+/* ---- GCN layer (gcn.hpp:91-193) ------------------------------------------ */
+/* gcn_forward: out (n x k) = A' X Theta + 1 b^T with the given scheme.  The
+ * returned cache borrows X (uncached schemes, gcn.hpp:111) -- X must stay
+ * valid until backward -- or owns P = A'X (propagate_first_cached). */
+int sgnn_gcn_forward(sgnn_ctx ctx, sgnn_adj adj, const void* X, int32_t m, const void* theta,
+                     const void* bias, int32_t k, const sgnn_scheme* scheme, void* out,
+                     sgnn_gcn_cache* cache);
+/* gcn_backward: consume-once cache (gcn.hpp:137-138: marked consumed before
+ * any other check); d_input may be NULL when needs_feature_grad == 0 */
+int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj adj, const void* d_out, const void* theta,
+                      int32_t m, int32_t k, sgnn_gcn_cache cache, int needs_feature_grad,
+                      void* d_theta, void* d_bias, void* d_input);
+int sgnn_gcn_cache_destroy(sgnn_gcn_cache cache);
+/* gcn.hpp:72-75 retained_bytes */
+int sgnn_gcn_cache_retained_bytes(sgnn_gcn_cache cache, int64_t* out);
+
+/* ---- GAT layer (gat.hpp:89-219) ------------------------------------------ */
+int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
+                     const void* a_src, const void* a_dst, const void* bias, int32_t heads,
+                     int32_t k, double beta, int level, int dtype, void* out,
+                     sgnn_gat_cache* cache);
+int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
+                      const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
+                      double beta, sgnn_gat_cache cache, int needs_feature_grad, void* d_theta,
+                      void* d_a_src, void* d_a_dst, void* d_bias, void* d_input);
+int sgnn_gat_cache_destroy(sgnn_gat_cache cache);
+/* gat.hpp:66-71 extra_bytes (== gat_cache_footprint at every level) */
+int sgnn_gat_cache_extra_bytes(sgnn_gat_cache cache, int64_t* out);
+/* cached (level full) or recomputed (gat.hpp:150-170) attention, converted to
+ * the reference head-major layout: alpha (h x q, dtype), mask (h x q bytes) */
+int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache cache,
+                               const void* theta, const void* a_src, const void* a_dst,
+                               void* alpha_hq, uint8_t* mask_hq);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* SGNN_CUDA_H */

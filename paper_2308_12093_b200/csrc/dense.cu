@@ -1,0 +1,323 @@
+// dense.cu -- dense pieces of the path (dense.hpp): the general GEMM used for
+// float64 (DFMA) and as the small-shape / non-tensor fallback, deterministic
+// column sums, and counter-based generation of the reference's random inputs.
+//
+// float32 X.Theta-class GEMMs go to the tcgen05 kernel in gemm_tc.cu when the
+// shape qualifies; this SIMT kernel handles float64 and odd shapes.
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace sgnn {
+
+// ---------------------------------------------------------------------------
+// SIMT GEMM: C[M x N] = op(A) op(B) (+bias), 64x64 tiles, 4x4 per thread,
+// optional split-K into float64/partial workspace reduced in a fixed order.
+// ---------------------------------------------------------------------------
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+template <class T, class Acc>
+__global__ void __launch_bounds__(256) k_gemm_simt(const T* __restrict__ A, const T* __restrict__ B,
+                                                   int M, int N, int K, int lda, int ldb, bool ta,
+                                                   bool tb, int kchunk, Acc* __restrict__ part,
+                                                   T* __restrict__ C, const T* __restrict__ bias) {
+  __shared__ T As[GBK][GBM + 4];
+  __shared__ T Bs[GBK][GBN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  const int k_begin = blockIdx.z * kchunk;
+  const int k_end = min(K, k_begin + kchunk);
+  Acc acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = Acc(0);
+
+  for (int k0 = k_begin; k0 < k_end; k0 += GBK) {
+    // A tile: GBM x GBK elements, 1024 / 256 = 4 per thread
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int idx = tid + t * 256;
+      int mm, kk;
+      if (ta) {  // A stored K x M: contiguous along m
+        mm = idx % GBM;
+        kk = idx / GBM;
+      } else {
+        kk = idx % GBK;
+        mm = idx / GBK;
+      }
+      const int gm = m0 + mm, gk = k0 + kk;
+      T v = T(0);
+      if (gm < M && gk < k_end) v = ta ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int idx = tid + t * 256;
+      int nn, kk;
+      if (tb) {  // B stored N x K: contiguous along k
+        kk = idx % GBK;
+        nn = idx / GBK;
+      } else {
+        nn = idx % GBN;
+        kk = idx / GBN;
+      }
+      const int gn = n0 + nn, gk = k0 + kk;
+      T v = T(0);
+      if (gn < N && gk < k_end) v = tb ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      Acc a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (Acc)As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = (Acc)Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < M && gn < N) {
+        if (part) {
+          part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+        } else {
+          T v = (T)acc[i][j];
+          if (bias) v = add_rn(v, bias[gn]);
+          C[(int64_t)gm * N + gn] = v;
+        }
+      }
+    }
+}
+
+template <class T, class Acc>
+__global__ void k_splitk_reduce(int splits, int64_t MN, int N, const Acc* __restrict__ part,
+                                T* __restrict__ C, const T* __restrict__ bias) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < MN;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += (double)part[(int64_t)z * MN + x];
+    T v = (T)s;
+    if (bias) v = add_rn(v, bias[x % N]);
+    C[x] = v;
+  }
+}
+
+template <class T>
+void gemm_simt(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int32_t rb,
+               int32_t cb, bool ta, bool tb, T* C, const T* bias) {
+  const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
+  if (M == 0 || N == 0) return;
+  const int tiles = (int)(ceil_div(M, GBM) * ceil_div(N, GBN));
+  int splits = 1;
+  const int target = 2 * ctx->num_sms;
+  if (tiles < target && K > 2048) {
+    splits = (int)std::min<int64_t>(ceil_div(target, tiles), ceil_div(K, 1024));
+    if (splits > 256) splits = 256;
+  }
+  int kchunk = (int)ceil_div(ceil_div(K, splits), GBK) * GBK;
+  if (K == 0) kchunk = GBK;
+  splits = K == 0 ? 1 : (int)ceil_div(K, kchunk);
+  dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)splits);
+  if (splits == 1) {
+    k_gemm_simt<T, T><<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
+                                                     (T*)nullptr, C, bias);
+    launched(ctx);
+  } else {
+    // float32 partials of <= kchunk terms, combined in float64 in slice order
+    using Acc = T;
+    DevBuf part((size_t)splits * M * N * sizeof(Acc), ctx->stream);
+    k_gemm_simt<T, Acc><<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
+                                                       part.as<Acc>(), C, bias);
+    launched(ctx);
+    const int64_t MN = (int64_t)M * N;
+    k_splitk_reduce<T, Acc><<<grid_for(ctx, MN, 256), 256, 0, ctx->stream>>>(
+        splits, MN, N, part.as<Acc>(), C, bias);
+    launched(ctx);
+  }
+}
+
+template void gemm_simt<float>(sgnn_ctx, const float*, int32_t, int32_t, const float*, int32_t,
+                               int32_t, bool, bool, float*, const float*);
+template void gemm_simt<double>(sgnn_ctx, const double*, int32_t, int32_t, const double*,
+                                int32_t, int32_t, bool, bool, double*, const double*);
+
+// tcgen05 path (gemm_tc.cu); returns false when the shape is not supported
+bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias);
+
+template <>
+void gemm<float>(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias) {
+  const int32_t kk = ta ? ra : ca, kb = tb ? cb : rb;
+  require(kk == kb, "gemm: inner dimensions do not match");
+  if (gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias)) return;
+  gemm_simt<float>(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias);
+}
+template <>
+void gemm<double>(sgnn_ctx ctx, const double* A, int32_t ra, int32_t ca, const double* B,
+                  int32_t rb, int32_t cb, bool ta, bool tb, double* C, const double* bias) {
+  const int32_t kk = ta ? ra : ca, kb = tb ? cb : rb;
+  require(kk == kb, "gemm: inner dimensions do not match");
+  gemm_simt<double>(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias);
+}
+
+// ---------------------------------------------------------------------------
+// column_sums (dense.hpp:272-282): row chunks accumulate in float64, chunk
+// partials are combined in chunk order -- deterministic, ~exact.
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void k_colsum_partial(const T* __restrict__ X, int32_t rows, int32_t cols,
+                                 int32_t chunk, double* __restrict__ part) {
+  const int32_t r0 = blockIdx.y * chunk;
+  const int32_t r1 = min(rows, r0 + chunk);
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int32_t i = r0; i < r1; ++i) s += (double)X[(int64_t)i * cols + j];
+    part[(int64_t)blockIdx.y * cols + j] = s;
+  }
+}
+
+template <class T>
+__global__ void k_colsum_final(int32_t nchunks, int32_t cols, const double* __restrict__ part,
+                               T* __restrict__ out) {
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int32_t c = 0; c < nchunks; ++c) s += part[(int64_t)c * cols + j];
+    out[j] = (T)s;
+  }
+}
+
+template <class T>
+void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out) {
+  if (cols == 0) return;
+  const int32_t chunk = 256;
+  const int32_t nchunks = rows > 0 ? (int32_t)ceil_div(rows, chunk) : 1;
+  DevBuf part((size_t)nchunks * cols * sizeof(double), ctx->stream);
+  dim3 g((unsigned)ceil_div(cols, 128), (unsigned)nchunks);
+  if (rows == 0) {
+    SGNN_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), ctx->stream));
+  } else {
+    k_colsum_partial<T><<<g, 128, 0, ctx->stream>>>(X, rows, cols, chunk, part.as<double>());
+    launched(ctx);
+  }
+  k_colsum_final<T><<<(unsigned)ceil_div(cols, 128), 128, 0, ctx->stream>>>(
+      nchunks, cols, part.as<double>(), out);
+  launched(ctx);
+}
+template void column_sums<float>(sgnn_ctx, const float*, int32_t, int32_t, float*);
+template void column_sums<double>(sgnn_ctx, const double*, int32_t, int32_t, double*);
+
+// ---------------------------------------------------------------------------
+// Counter-based form of the reference RNG (rng.hpp:13-42): after Rng(seed)
+// the i-th next_u64() mixes seed + (i + 2) * golden, so every draw of
+// DenseMatrix::random_uniform (dense.hpp:45-53) is computed independently on
+// the device, bit-identical to the sequential host stream.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 2) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void k_random_uniform(int64_t count, uint64_t seed, double lo, double hi, T* out) {
+  const double span = __dsub_rn(hi, lo);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = __dmul_rn((double)(splitmix_at(seed, (uint64_t)i) >> 11), 0x1.0p-53);
+    out[i] = (T)__dadd_rn(lo, __dmul_rn(span, u));
+  }
+}
+
+template <class T>
+void random_uniform(sgnn_ctx ctx, int64_t count, uint64_t seed, double lo, double hi, T* out) {
+  if (count == 0) return;
+  k_random_uniform<T><<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(count, seed, lo, hi,
+                                                                          out);
+  launched(ctx);
+}
+template void random_uniform<float>(sgnn_ctx, int64_t, uint64_t, double, double, float*);
+template void random_uniform<double>(sgnn_ctx, int64_t, uint64_t, double, double, double*);
+
+}  // namespace sgnn
+
+using namespace sgnn;
+
+#define DISPATCH_T(dtype, ...)                 \
+  do {                                         \
+    if ((dtype) == SGNN_F32) {                 \
+      using T = float;                         \
+      __VA_ARGS__;                             \
+    } else if ((dtype) == SGNN_F64) {          \
+      using T = double;                        \
+      __VA_ARGS__;                             \
+    } else {                                   \
+      throw invalid_argument("unknown dtype"); \
+    }                                          \
+  } while (0)
+
+extern "C" {
+
+int sgnn_gemm(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+              int32_t rb, int32_t cb, int ta, int tb, void* C) {
+  SGNN_API_BEGIN
+  DISPATCH_T(dtype, gemm<T>(ctx, static_cast<const T*>(A), ra, ca, static_cast<const T*>(B), rb,
+                            cb, ta != 0, tb != 0, static_cast<T*>(C), nullptr));
+  SGNN_API_END
+}
+
+int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
+                     void* out) {
+  SGNN_API_BEGIN
+  DISPATCH_T(dtype, column_sums<T>(ctx, static_cast<const T*>(X), rows, cols,
+                                   static_cast<T*>(out)));
+  SGNN_API_END
+}
+
+int sgnn_random_uniform(sgnn_ctx ctx, int64_t rows, int64_t cols, uint64_t seed, double lo,
+                        double hi, int dtype, void* out) {
+  SGNN_API_BEGIN
+  DISPATCH_T(dtype, random_uniform<T>(ctx, rows * cols, seed, lo, hi, static_cast<T*>(out)));
+  SGNN_API_END
+}
+
+// gcn.hpp:54-62 -- bound = 1/sqrt(m) in double, theta from seed, bias Rng(seed+1)
+int sgnn_gcn_params_init(sgnn_ctx ctx, int32_t m, int32_t k, uint64_t seed, int dtype,
+                         void* theta, void* bias) {
+  SGNN_API_BEGIN
+  const double bound = 1.0 / std::sqrt((double)m);
+  DISPATCH_T(dtype, {
+    random_uniform<T>(ctx, (int64_t)m * k, seed, -bound, bound, static_cast<T*>(theta));
+    random_uniform<T>(ctx, k, seed + 1, -bound, bound, static_cast<T*>(bias));
+  });
+  SGNN_API_END
+}
+
+// gat.hpp:36-52
+int sgnn_gat_params_init(sgnn_ctx ctx, int32_t m, int32_t h, int32_t k, uint64_t seed,
+                         int dtype, void* theta, void* a_src, void* a_dst, void* bias) {
+  SGNN_API_BEGIN
+  require(h >= 1, "GatParams: heads must be >= 1");
+  const double bound = 1.0 / std::sqrt((double)m);
+  const double abound = 1.0 / std::sqrt((double)k);
+  DISPATCH_T(dtype, {
+    random_uniform<T>(ctx, (int64_t)m * h * k, seed, -bound, bound, static_cast<T*>(theta));
+    random_uniform<T>(ctx, (int64_t)h * k, seed + 1, -abound, abound, static_cast<T*>(a_src));
+    random_uniform<T>(ctx, (int64_t)h * k, seed + 2, -abound, abound, static_cast<T*>(a_dst));
+    random_uniform<T>(ctx, (int64_t)h * k, seed + 3, -bound, bound, static_cast<T*>(bias));
+  });
+  SGNN_API_END
+}
+
+}  // extern "C"

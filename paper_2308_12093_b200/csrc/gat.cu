@@ -1,0 +1,851 @@
+// gat.cu -- GAT engine (north-star subsystem 3; gat.hpp:89-219, kernels.hpp:383-658).
+//
+// Forward: M = X Theta (GEMM) -> node scores s, d -> ONE fused row kernel per
+// destination node (warp per row): per-head row max and 1/sum of exp
+// (LeakyReLU(s_i + d_j) computed on the fly, never materialised), then
+// batches of (edge, head) attention coefficients staged in shared memory and
+// the multi-head aggregation out[i] = sum_e alpha_e M[j] + b with 128-bit
+// loads of the M rows.  alpha + mask are written only at cache level `full`.
+//
+// Backward: row kernel (SDDMM dAlpha = <dX'_i, M_j> per (edge, head), softmax
+// and LeakyReLU backward, row sums dS) -> column kernel over the CSC view
+// (dD = column sums, dM = alpha^T dX' + dS a_src + dD a_dst) -> attention
+// parameter reductions -> dTheta = X^T dM, dX = dM Theta^T (GEMMs).
+//
+// Order of accumulation follows the reference per output element (edge order,
+// unfused multiply-add), so float64 results agree with the reference to a
+// few ulps (exp() differs from glibc by <= 1 ulp).
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace sgnn {
+
+constexpr int HMAX = 64;  // heads supported by the fused kernels
+
+template <class T>
+__device__ __forceinline__ T dev_exp(T x);
+template <>
+__device__ __forceinline__ float dev_exp<float>(float x) {
+  return expf(x);
+}
+template <>
+__device__ __forceinline__ double dev_exp<double>(double x) {
+  return exp(x);
+}
+
+template <class T>
+__device__ __forceinline__ T leaky(T y, T beta, bool& pos) {
+  pos = y > T(0);  // kernels.hpp:473-475
+  return pos ? y : mul_rn(beta, y);
+}
+
+template <class T, int W>
+struct V;
+template <class T>
+struct V<T, 1> {
+  using t = T;
+};
+template <>
+struct V<float, 4> {
+  using t = float4;
+};
+template <>
+struct V<double, 2> {
+  using t = double2;
+};
+
+template <class T, int W>
+__device__ __forceinline__ void vload(const T* p, T (&out)[W]) {
+  using VT = typename V<T, W>::t;
+  const VT v = __ldg(reinterpret_cast<const VT*>(p));
+  const T* q = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int w = 0; w < W; ++w) out[w] = q[w];
+}
+template <class T, int W>
+__device__ __forceinline__ void vstore(T* p, const T (&in)[W]) {
+  using VT = typename V<T, W>::t;
+  VT v;
+  T* q = reinterpret_cast<T*>(&v);
+#pragma unroll
+  for (int w = 0; w < W; ++w) q[w] = in[w];
+  *reinterpret_cast<VT*>(p) = v;
+}
+
+// kernels.hpp:385-423 node_scores: one thread per (node, head), sequential dot
+template <class T>
+__global__ void k_node_scores(int32_t n, int32_t h, int32_t k, const T* __restrict__ M,
+                              const T* __restrict__ a_src, const T* __restrict__ a_dst,
+                              T* __restrict__ s, T* __restrict__ d) {
+  const int64_t total = (int64_t)n * h;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = (int32_t)(x % h);
+    const T* mrow = M + x * k;
+    const T* as = a_src + (int64_t)t * k;
+    const T* ad = a_dst + (int64_t)t * k;
+    T sv = T(0), dv = T(0);
+    for (int32_t c = 0; c < k; ++c) {
+      const T mv = mrow[c];
+      sv = madd(sv, __ldg(as + c), mv);
+      dv = madd(dv, __ldg(ad + c), mv);
+    }
+    s[x] = sv;
+    d[x] = dv;
+  }
+}
+
+struct WarpSmem {
+  static constexpr int kAlpha = 64;
+};
+
+// Per-row softmax statistics (kernels.hpp:517-531): lanes own heads and walk
+// the row in stored order, exactly like the reference loop.
+template <class T>
+__device__ __forceinline__ void row_stats(int lane, int32_t i, int32_t beg, int32_t end,
+                                          const int32_t* __restrict__ cols,
+                                          const T* __restrict__ s, const T* __restrict__ d,
+                                          int32_t h, T beta, T* smax, T* sinv) {
+  for (int t = lane; t < h; t += 32) {
+    const T si = s[(int64_t)i * h + t];
+    bool pos;
+    T gmax = leaky(add_rn(si, d[(int64_t)__ldg(cols + beg) * h + t]), beta, pos);
+    for (int32_t e = beg + 1; e < end; ++e) {
+      const T w = leaky(add_rn(si, d[(int64_t)__ldg(cols + e) * h + t]), beta, pos);
+      gmax = gmax < w ? w : gmax;
+    }
+    T sum = T(0);
+    for (int32_t e = beg; e < end; ++e) {
+      const T w = leaky(add_rn(si, d[(int64_t)__ldg(cols + e) * h + t]), beta, pos);
+      sum = add_rn(sum, dev_exp<T>(w - gmax));
+    }
+    smax[t] = gmax;
+    sinv[t] = T(1) / sum;
+  }
+}
+
+// Fused attention + aggregation. W scalars per vector, R vectors per lane per
+// column block.  STORE: write alpha/mask (edge-major). AGG: aggregate.
+template <class T, int W, int R, bool STORE, bool AGG>
+__global__ void __launch_bounds__(256) k_gat_fwd(int32_t n, const int32_t* __restrict__ rowptr,
+                                                 const int32_t* __restrict__ cols,
+                                                 const T* __restrict__ M, const T* __restrict__ s,
+                                                 const T* __restrict__ d, int32_t h, int32_t k,
+                                                 T beta, const T* __restrict__ bias,
+                                                 T* __restrict__ out, T* __restrict__ alpha,
+                                                 uint8_t* __restrict__ mask) {
+  __shared__ T sh_max[8][HMAX];
+  __shared__ T sh_inv[8][HMAX];
+  __shared__ T sh_al[8][HMAX];
+  __shared__ int32_t sh_col[8][32];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* smax = sh_max[wib];
+  T* sinv = sh_inv[wib];
+  T* sal = sh_al[wib];
+  int32_t* scol = sh_col[wib];
+  const int32_t hk = h * k;
+  const int fv = hk / W;
+  int hp = 1;
+  while (hp < h) hp <<= 1;
+  const int EB = hp >= 32 ? 1 : 32 / hp;  // edges per batch
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  for (int64_t ii = warp; ii < n; ii += nwarps) {
+    const int32_t i = (int32_t)ii;
+    const int32_t beg = rowptr[i], end = rowptr[i + 1];
+    row_stats<T>(lane, i, beg, end, cols, s, d, h, beta, smax, sinv);
+    __syncwarp();
+    const int ncb = AGG ? (int)ceil_div(fv, 32 * R) : 1;
+    for (int cb = 0; cb < ncb; ++cb) {
+      T acc[R][W];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[r][w] = T(0);
+      for (int32_t base = beg; base < end; base += EB) {
+        const int cnt = min(EB, end - base);
+        for (int idx = lane; idx < EB * hp; idx += 32) {
+          const int eb = idx / hp, t = idx % hp;
+          if (t < h && eb < cnt) {
+            const int32_t e = base + eb;
+            const int32_t j = __ldg(cols + e);
+            bool pos;
+            const T w = leaky(add_rn(s[(int64_t)i * h + t], d[(int64_t)j * h + t]), beta, pos);
+            const T a = mul_rn(dev_exp<T>(w - smax[t]), sinv[t]);
+            sal[eb * hp + t] = a;
+            if (STORE && cb == 0) {
+              alpha[(int64_t)e * h + t] = a;
+              mask[(int64_t)e * h + t] = pos ? 1 : 0;
+            }
+          }
+        }
+        if (lane < cnt) scol[lane] = __ldg(cols + base + lane);
+        __syncwarp();
+        if (AGG) {
+          for (int eb = 0; eb < cnt; ++eb) {
+            const T* mrow = M + (int64_t)scol[eb] * hk;
+            T mv[R][W];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int v = cb * 32 * R + r * 32 + lane;
+              if (v < fv) vload<T, W>(mrow + (int64_t)v * W, mv[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int v = cb * 32 * R + r * 32 + lane;
+              if (v < fv) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                  const int c = v * W + w;
+                  acc[r][w] = madd(acc[r][w], sal[eb * hp + c / k], mv[r][w]);
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (AGG) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int v = cb * 32 * R + r * 32 + lane;
+          if (v < fv) {
+            T b[W], o[W];
+            vload<T, W>(bias + (int64_t)v * W, b);
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = add_rn(acc[r][w], b[w]);
+            vstore<T, W>(out + (int64_t)i * hk + (int64_t)v * W, o);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Backward, per destination row: alpha (cached or recomputed), dAlpha (SDDMM,
+// kernels.hpp:342-377), softmax backward (:537-567), LeakyReLU backward
+// (:481-495), row sums dS (:570-588).  dy and alpha written edge-major.
+template <class T, int W, bool CACHED>
+__global__ void __launch_bounds__(256) k_gat_bwd_row(
+    int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+    const T* __restrict__ M, const T* __restrict__ s, const T* __restrict__ d,
+    const T* __restrict__ G, int32_t h, int32_t k, T beta, const T* __restrict__ alpha_in,
+    const uint8_t* __restrict__ mask_in, T* __restrict__ alpha_out,
+    uint8_t* __restrict__ mask_out, T* __restrict__ da, T* __restrict__ dy,
+    T* __restrict__ dS) {
+  __shared__ T sh_max[8][HMAX];
+  __shared__ T sh_inv[8][HMAX];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* smax = sh_max[wib];
+  T* sinv = sh_inv[wib];
+  const int32_t hk = h * k;
+  int hp = 1;
+  while (hp < h) hp <<= 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T* al = CACHED ? alpha_in : alpha_out;
+  const uint8_t* mk = CACHED ? mask_in : mask_out;
+
+  for (int64_t ii = warp; ii < n; ii += nwarps) {
+    const int32_t i = (int32_t)ii;
+    const int32_t beg = rowptr[i], end = rowptr[i + 1];
+    if (!CACHED) {
+      row_stats<T>(lane, i, beg, end, cols, s, d, h, beta, smax, sinv);
+      __syncwarp();
+    }
+    const T* grow = G + (int64_t)i * hk;
+    const int64_t pairs = (int64_t)(end - beg) * hp;
+    for (int64_t idx = lane; idx < pairs; idx += 32) {
+      const int32_t e = beg + (int32_t)(idx / hp);
+      const int t = (int)(idx % hp);
+      if (t >= h) continue;
+      const int32_t j = __ldg(cols + e);
+      if (!CACHED) {
+        bool pos;
+        const T w = leaky(add_rn(s[(int64_t)i * h + t], d[(int64_t)j * h + t]), beta, pos);
+        alpha_out[(int64_t)e * h + t] = mul_rn(dev_exp<T>(w - smax[t]), sinv[t]);
+        mask_out[(int64_t)e * h + t] = pos ? 1 : 0;
+      }
+      const T* gr = grow + (int64_t)t * k;
+      const T* mr = M + (int64_t)j * hk + (int64_t)t * k;
+      T acc = T(0);
+      for (int32_t c = 0; c < k; c += W) {
+        T gv[W], mv[W];
+        vload<T, W>(gr + c, gv);
+        vload<T, W>(mr + c, mv);
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc = madd(acc, gv[w], mv[w]);
+      }
+      da[(int64_t)e * h + t] = acc;
+    }
+    __syncwarp();
+    for (int t = lane; t < h; t += 32) {
+      T dot = T(0);
+      for (int32_t e = beg; e < end; ++e)
+        dot = madd(dot, al[(int64_t)e * h + t], da[(int64_t)e * h + t]);
+      T rs = T(0);
+      for (int32_t e = beg; e < end; ++e) {
+        const T a = al[(int64_t)e * h + t];
+        const T dw = mul_rn(a, da[(int64_t)e * h + t] - dot);
+        const T g = mk[(int64_t)e * h + t] ? dw : mul_rn(beta, dw);
+        dy[(int64_t)e * h + t] = g;
+        rs = add_rn(rs, g);
+      }
+      dS[(int64_t)i * h + t] = rs;
+    }
+    __syncwarp();
+  }
+}
+
+// Backward, per source column j over the CSC view: dD (kernels.hpp:639-658)
+// and dM = alpha^T dX' (:258-295) + dS a_src + dD a_dst (:614-636).
+template <class T, int W, int R>
+__global__ void __launch_bounds__(256) k_gat_bwd_col(
+    int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
+    const int32_t* __restrict__ perm, const T* __restrict__ G, const T* __restrict__ alpha,
+    const T* __restrict__ dy, const T* __restrict__ dS, const T* __restrict__ a_src,
+    const T* __restrict__ a_dst, int32_t h, int32_t k, T* __restrict__ dD, T* __restrict__ dM) {
+  __shared__ T sh_dd[8][HMAX];
+  __shared__ T sh_al[8][HMAX];
+  __shared__ int32_t sh_row[8][32];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* sdd = sh_dd[wib];
+  T* sal = sh_al[wib];
+  int32_t* srow = sh_row[wib];
+  const int32_t hk = h * k;
+  const int fv = hk / W;
+  int hp = 1;
+  while (hp < h) hp <<= 1;
+  const int EB = hp >= 32 ? 1 : 32 / hp;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+
+  for (int64_t jj = warp; jj < n; jj += nwarps) {
+    const int32_t j = (int32_t)jj;
+    const int32_t beg = colptr[j], end = colptr[j + 1];
+    for (int t = lane; t < h; t += 32) {
+      T acc = T(0);
+      for (int32_t p = beg; p < end; ++p) acc = add_rn(acc, dy[(int64_t)__ldg(perm + p) * h + t]);
+      sdd[t] = acc;
+      dD[(int64_t)j * h + t] = acc;
+    }
+    __syncwarp();
+    const int ncb = (int)ceil_div(fv, 32 * R);
+    for (int cb = 0; cb < ncb; ++cb) {
+      T acc[R][W];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[r][w] = T(0);
+      for (int32_t base = beg; base < end; base += EB) {
+        const int cnt = min(EB, end - base);
+        for (int idx = lane; idx < EB * hp; idx += 32) {
+          const int eb = idx / hp, t = idx % hp;
+          if (t < h && eb < cnt) sal[eb * hp + t] = alpha[(int64_t)__ldg(perm + base + eb) * h + t];
+        }
+        if (lane < cnt) srow[lane] = __ldg(crows + base + lane);
+        __syncwarp();
+        for (int eb = 0; eb < cnt; ++eb) {
+          const T* grow = G + (int64_t)srow[eb] * hk;
+          T gv[R][W];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int v = cb * 32 * R + r * 32 + lane;
+            if (v < fv) vload<T, W>(grow + (int64_t)v * W, gv[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int v = cb * 32 * R + r * 32 + lane;
+            if (v < fv) {
+#pragma unroll
+              for (int w = 0; w < W; ++w)
+                acc[r][w] = madd(acc[r][w], sal[eb * hp + (v * W + w) / k], gv[r][w]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int v = cb * 32 * R + r * 32 + lane;
+        if (v < fv) {
+          T o[W];
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const int c = v * W + w;
+            const int t = c / k, cc = c % k;
+            T x = madd(acc[r][w], dS[(int64_t)j * h + t], __ldg(a_src + (int64_t)t * k + cc));
+            o[w] = madd(x, sdd[t], __ldg(a_dst + (int64_t)t * k + cc));
+          }
+          vstore<T, W>(dM + (int64_t)j * hk + (int64_t)v * W, o);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// attention_param_grad (kernels.hpp:592-611): out[t,c] = sum_i coeff[i,t] M[i,t,c]
+template <class T>
+__global__ void k_attgrad_partial(int32_t n, int32_t h, int32_t k, const T* __restrict__ M,
+                                  const T* __restrict__ coeff, int32_t chunk,
+                                  double* __restrict__ part) {
+  const int32_t hk = h * k;
+  const int32_t r0 = blockIdx.y * chunk, r1 = min(n, r0 + chunk);
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < hk; c += gridDim.x * blockDim.x) {
+    const int32_t t = c / k;
+    double acc = 0.0;
+    for (int32_t i = r0; i < r1; ++i)
+      acc += (double)coeff[(int64_t)i * h + t] * (double)M[(int64_t)i * hk + c];
+    part[(int64_t)blockIdx.y * hk + c] = acc;
+  }
+}
+
+template <class T>
+__global__ void k_attgrad_final(int32_t nchunks, int32_t hk, const double* __restrict__ part,
+                                T* __restrict__ out) {
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < hk; c += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int32_t z = 0; z < nchunks; ++z) s += part[(int64_t)z * hk + c];
+    out[c] = (T)s;
+  }
+}
+
+template <class T>
+__global__ void k_edge_to_head_major(int64_t q, int32_t h, const T* __restrict__ eq,
+                                     const uint8_t* __restrict__ mq, T* __restrict__ hq,
+                                     uint8_t* __restrict__ mh) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < q * h;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = x / h, t = x % h;
+    if (hq) hq[t * q + e] = eq[x];
+    if (mh) mh[t * q + e] = mq[x];
+  }
+}
+
+// kernels.hpp:500-534 edge_softmax over arbitrary scores (edge-major q x h)
+template <class T>
+__global__ void k_edge_softmax(int32_t n, const int32_t* __restrict__ rowptr, int32_t h,
+                               const T* __restrict__ w, T* __restrict__ alpha) {
+  const int64_t total = (int64_t)n * h;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = (int32_t)(x / h), t = (int32_t)(x % h);
+    const int32_t beg = rowptr[i], end = rowptr[i + 1];
+    T gmax = w[(int64_t)beg * h + t];
+    for (int32_t e = beg + 1; e < end; ++e) {
+      const T v = w[(int64_t)e * h + t];
+      gmax = gmax < v ? v : gmax;
+    }
+    T sum = T(0);
+    for (int32_t e = beg; e < end; ++e) sum = add_rn(sum, dev_exp<T>(w[(int64_t)e * h + t] - gmax));
+    const T inv = T(1) / sum;
+    for (int32_t e = beg; e < end; ++e)
+      alpha[(int64_t)e * h + t] = mul_rn(dev_exp<T>(w[(int64_t)e * h + t] - gmax), inv);
+  }
+}
+
+// kernels.hpp:301-337 sddmm (one head, no scale): thread per edge, sequential dot
+template <class T>
+__global__ void k_sddmm(int32_t n, const int32_t* __restrict__ rowptr,
+                        const int32_t* __restrict__ cols, const T* __restrict__ B, int32_t f,
+                        const T* __restrict__ C, int32_t ldc, T* __restrict__ out) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const T* brow = B + i * f;
+    for (int32_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) {
+      const int32_t j = cols[e];
+      T acc = T(0);
+      for (int32_t l = 0; l < f; ++l) acc = madd(acc, brow[l], C[(int64_t)l * ldc + j]);
+      out[e] = acc;
+    }
+  }
+}
+
+// ---- host launchers ---------------------------------------------------------
+static int pick_r(int fv) {
+  const int need = (int)ceil_div(fv, 32);
+  return need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : need <= 8 ? 8 : 16;
+}
+
+template <class T, int W, bool STORE, bool AGG>
+static void launch_fwd_w(sgnn_ctx ctx, int32_t n, const int32_t* rp, const int32_t* ci,
+                         const T* M, const T* s, const T* d, int32_t h, int32_t k, T beta,
+                         const T* bias, T* out, T* alpha, uint8_t* mask) {
+  const int R = AGG ? pick_r(h * k / W) : 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8),
+                                                               (int64_t)ctx->num_sms * 32));
+  switch (R) {
+#define CASE(RR)                                                                             \
+  case RR:                                                                                   \
+    k_gat_fwd<T, W, RR, STORE, AGG><<<grid, 256, 0, ctx->stream>>>(n, rp, ci, M, s, d, h, k,    \
+                                                                  beta, bias, out, alpha, mask); \
+    break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+#undef CASE
+  }
+  launched(ctx);
+}
+
+template <class T, bool STORE, bool AGG>
+static void launch_fwd(sgnn_ctx ctx, int32_t n, const int32_t* rp, const int32_t* ci,
+                       const T* M, const T* s, const T* d, int32_t h, int32_t k, T beta,
+                       const T* bias, T* out, T* alpha, uint8_t* mask) {
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  const bool vec = k % VW == 0 && reinterpret_cast<uintptr_t>(M) % 16 == 0 &&
+                   (!AGG || (reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                             reinterpret_cast<uintptr_t>(bias) % 16 == 0));
+  if (vec)
+    launch_fwd_w<T, VW, STORE, AGG>(ctx, n, rp, ci, M, s, d, h, k, beta, bias, out, alpha, mask);
+  else
+    launch_fwd_w<T, 1, STORE, AGG>(ctx, n, rp, ci, M, s, d, h, k, beta, bias, out, alpha, mask);
+}
+
+template <class T>
+static void node_scores(sgnn_ctx ctx, int32_t n, int32_t h, int32_t k, const T* M,
+                        const T* a_src, const T* a_dst, T* s, T* d) {
+  k_node_scores<T><<<grid_for(ctx, (int64_t)n * h, 256), 256, 0, ctx->stream>>>(n, h, k, M, a_src,
+                                                                               a_dst, s, d);
+  launched(ctx);
+}
+
+template <class T>
+static void att_grad(sgnn_ctx ctx, int32_t n, int32_t h, int32_t k, const T* M, const T* coeff,
+                     T* out) {
+  const int32_t hk = h * k, chunk = 512;
+  const int32_t nch = std::max<int32_t>(1, (int32_t)ceil_div(n, chunk));
+  DevBuf part((size_t)nch * hk * 8, ctx->stream);
+  if (n == 0) SGNN_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), ctx->stream));
+  else {
+    dim3 g((unsigned)ceil_div(hk, 128), (unsigned)nch);
+    k_attgrad_partial<T><<<g, 128, 0, ctx->stream>>>(n, h, k, M, coeff, chunk, part.as<double>());
+    launched(ctx);
+  }
+  k_attgrad_final<T><<<(unsigned)ceil_div(hk, 128), 128, 0, ctx->stream>>>(nch, hk,
+                                                                           part.as<double>(), out);
+  launched(ctx);
+}
+
+template <class T>
+static int rows_grid(sgnn_ctx ctx, int32_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (int64_t)ctx->num_sms * 32));
+}
+
+template <class T>
+void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T* theta,
+                   const T* a_src, const T* a_dst, const T* bias, int32_t h, int32_t k,
+                   T beta, int level, T* out, sgnn_gat_cache c) {
+  const int32_t n = p->n;
+  const int64_t q = p->nnz;
+  const int32_t hk = h * k;
+  cudaStream_t st = ctx->stream;
+  DevBuf M((size_t)n * hk * sizeof(T), st), s((size_t)n * h * sizeof(T) + 8, st),
+      d((size_t)n * h * sizeof(T) + 8, st), alpha, mask;
+  gemm<T>(ctx, X, n, m, theta, m, hk, false, false, M.as<T>());
+  node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+  const int32_t* rp = p->rowptr.as<int32_t>();
+  const int32_t* ci = p->cols.as<int32_t>();
+  if (level == SGNN_GAT_FULL) {
+    alpha = DevBuf((size_t)q * h * sizeof(T) + 8, st);
+    mask = DevBuf((size_t)q * h + 8, st);
+    launch_fwd<T, true, true>(ctx, n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias,
+                              out, alpha.as<T>(), mask.as<uint8_t>());
+  } else {
+    launch_fwd<T, false, true>(ctx, n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta,
+                               bias, out, nullptr, nullptr);
+  }
+  // reclassify retained buffers into the cache (gat.hpp:123-137)
+  c->saved_input = X;
+  if (level >= SGNN_GAT_FEATURES) c->M = std::move(M);
+  if (level == SGNN_GAT_NODE_ATTENTION) {
+    c->s = std::move(s);
+    c->d = std::move(d);
+  }
+  if (level == SGNN_GAT_FULL) {
+    c->alpha = std::move(alpha);
+    c->mask = std::move(mask);
+  }
+}
+
+// gat.hpp:150-170 gat_recompute of the pieces the level did not keep
+template <class T>
+struct Recomputed {
+  DevBuf M, s, d;
+  const T* Mp = nullptr;
+  const T* sp = nullptr;
+  const T* dp = nullptr;
+};
+
+template <class T>
+static void recompute(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* theta,
+                      const T* a_src, const T* a_dst, Recomputed<T>& r) {
+  const int32_t n = p->n, h = c->h, k = c->k, hk = h * k;
+  cudaStream_t st = ctx->stream;
+  if (c->level >= SGNN_GAT_FEATURES) {
+    r.Mp = c->M.as<T>();
+  } else {
+    r.M = DevBuf((size_t)n * hk * sizeof(T), st);
+    gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, c->m, theta, c->m, hk, false, false,
+            r.M.template as<T>());
+    r.Mp = r.M.template as<T>();
+  }
+  if (c->level == SGNN_GAT_FULL) return;
+  if (c->level == SGNN_GAT_NODE_ATTENTION) {
+    r.sp = c->s.as<T>();
+    r.dp = c->d.as<T>();
+  } else {
+    r.s = DevBuf((size_t)n * h * sizeof(T) + 8, st);
+    r.d = DevBuf((size_t)n * h * sizeof(T) + 8, st);
+    node_scores<T>(ctx, n, h, k, r.Mp, a_src, a_dst, r.s.template as<T>(), r.d.template as<T>());
+    r.sp = r.s.template as<T>();
+    r.dp = r.d.template as<T>();
+  }
+}
+
+template <class T>
+void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, const T* a_src,
+                    const T* a_dst, sgnn_gat_cache c, bool fg, T* d_theta, T* d_a_src,
+                    T* d_a_dst, T* d_bias, T* d_input) {
+  const int32_t n = p->n, h = c->h, k = c->k, hk = h * k, m = c->m;
+  const int64_t q = p->nnz;
+  const T beta = (T)c->beta;
+  cudaStream_t st = ctx->stream;
+  column_sums<T>(ctx, G, n, hk, d_bias);
+  Recomputed<T> r;
+  recompute<T>(ctx, p, c, theta, a_src, a_dst, r);
+  const bool cached = c->level == SGNN_GAT_FULL;
+  DevBuf alpha_t, mask_t, da((size_t)q * h * sizeof(T) + 8, st), dy((size_t)q * h * sizeof(T) + 8, st),
+      dS((size_t)n * h * sizeof(T) + 8, st), dD((size_t)n * h * sizeof(T) + 8, st),
+      dM((size_t)n * hk * sizeof(T), st);
+  if (!cached) {
+    alpha_t = DevBuf((size_t)q * h * sizeof(T) + 8, st);
+    mask_t = DevBuf((size_t)q * h + 8, st);
+  }
+  const T* alpha = cached ? c->alpha.as<T>() : alpha_t.as<T>();
+  const int32_t* rp = p->rowptr.as<int32_t>();
+  const int32_t* ci = p->cols.as<int32_t>();
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  const bool vec = k % VW == 0 && reinterpret_cast<uintptr_t>(G) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(r.Mp) % 16 == 0;
+  const int g = rows_grid<T>(ctx, n);
+#define ROW(W, CACHED)                                                                        \
+  k_gat_bwd_row<T, W, CACHED><<<g, 256, 0, st>>>(n, rp, ci, r.Mp, r.sp, r.dp, G, h, k, beta,  \
+                                                c->alpha.as<T>(), c->mask.as<uint8_t>(),       \
+                                                alpha_t.as<T>(), mask_t.as<uint8_t>(),        \
+                                                da.as<T>(), dy.as<T>(), dS.as<T>())
+  if (vec) {
+    if (cached) ROW(VW, true); else ROW(VW, false);
+  } else {
+    if (cached) ROW(1, true); else ROW(1, false);
+  }
+#undef ROW
+  launched(ctx);
+  // column pass over the CSC view
+  const int32_t* cp = p->colptr.as<int32_t>();
+  const int32_t* cr = p->rows.as<int32_t>();
+  const int32_t* pm = p->perm.as<int32_t>();
+  const bool cvec = vec && reinterpret_cast<uintptr_t>(dM.get()) % 16 == 0;
+  const int W = cvec ? VW : 1;
+  const int R = pick_r(hk / W);
+#define COL(WW, RR)                                                                            \
+  k_gat_bwd_col<T, WW, RR><<<g, 256, 0, st>>>(n, cp, cr, pm, G, alpha, dy.as<T>(), dS.as<T>(), \
+                                             a_src, a_dst, h, k, dD.as<T>(), dM.as<T>())
+#define COLR(WW)                    \
+  switch (R) {                      \
+    case 1: COL(WW, 1); break;      \
+    case 2: COL(WW, 2); break;      \
+    case 4: COL(WW, 4); break;      \
+    case 8: COL(WW, 8); break;      \
+    default: COL(WW, 16); break;    \
+  }
+  if (W == VW) {
+    COLR(VW)
+  } else {
+    COLR(1)
+  }
+#undef COLR
+#undef COL
+  launched(ctx);
+  att_grad<T>(ctx, n, h, k, r.Mp, dS.as<T>(), d_a_src);
+  att_grad<T>(ctx, n, h, k, r.Mp, dD.as<T>(), d_a_dst);
+  gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
+          d_theta);
+  if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+}
+
+template <class T>
+void gat_edge_values_t(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* theta,
+                       const T* a_src, const T* a_dst, T* alpha_hq, uint8_t* mask_hq) {
+  const int32_t n = p->n, h = c->h, k = c->k;
+  const int64_t q = p->nnz;
+  cudaStream_t st = ctx->stream;
+  DevBuf al, mk;
+  const T* ae;
+  const uint8_t* me;
+  if (c->level == SGNN_GAT_FULL) {
+    ae = c->alpha.as<T>();
+    me = c->mask.as<uint8_t>();
+  } else {
+    Recomputed<T> r;
+    recompute<T>(ctx, p, c, theta, a_src, a_dst, r);
+    al = DevBuf((size_t)q * h * sizeof(T) + 8, st);
+    mk = DevBuf((size_t)q * h + 8, st);
+    launch_fwd<T, true, false>(ctx, n, p->rowptr.as<int32_t>(), p->cols.as<int32_t>(), r.Mp,
+                               r.sp, r.dp, h, k, (T)c->beta, nullptr, nullptr, al.as<T>(),
+                               mk.as<uint8_t>());
+    ae = al.as<T>();
+    me = mk.as<uint8_t>();
+  }
+  k_edge_to_head_major<T><<<grid_for(ctx, q * h, 256), 256, 0, st>>>(q, h, ae, me, alpha_hq,
+                                                                     mask_hq);
+  launched(ctx);
+}
+
+}  // namespace sgnn
+
+using namespace sgnn;
+
+extern "C" {
+
+int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
+                     const void* a_src, const void* a_dst, const void* bias, int32_t heads,
+                     int32_t k, double beta, int level, int dtype, void* out,
+                     sgnn_gat_cache* cache) {
+  SGNN_API_BEGIN
+  require(p && p->all_self_loops, "gat_forward: pattern must contain all self loops");
+  require(m >= 1 && heads >= 1 && k >= 1, "gat_forward: input width does not match theta");
+  require(beta > 0, "gat_forward: beta must be positive");
+  require(heads <= HMAX, "gat_forward: more than 64 heads is not supported on the device");
+  require(level >= SGNN_GAT_NONE && level <= SGNN_GAT_FULL, "unknown caching level");
+  auto* c = new sgnn_gat_cache_s;
+  c->level = level;
+  c->dtype = dtype;
+  c->n = p->n;
+  c->m = m;
+  c->h = heads;
+  c->k = k;
+  c->beta = beta;
+  try {
+    if (dtype == SGNN_F32)
+      gat_forward_t<float>(ctx, p, (const float*)X, m, (const float*)theta, (const float*)a_src,
+                           (const float*)a_dst, (const float*)bias, heads, k, (float)beta, level,
+                           (float*)out, c);
+    else if (dtype == SGNN_F64)
+      gat_forward_t<double>(ctx, p, (const double*)X, m, (const double*)theta,
+                            (const double*)a_src, (const double*)a_dst, (const double*)bias,
+                            heads, k, beta, level, (double*)out, c);
+    else
+      throw invalid_argument("unknown dtype");
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *cache = c;
+  SGNN_API_END
+}
+
+int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
+                      const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
+                      double beta, sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src,
+                      void* d_a_dst, void* d_bias, void* d_input) {
+  SGNN_API_BEGIN
+  require(c != nullptr, "gat_backward: missing saved input");
+  require(!c->consumed, "gat_backward: cache already consumed");
+  c->consumed = true;  // gat.hpp:177-178
+  require(p && p->n == c->n && heads == c->h && k == c->k,
+          "gat_backward: gradient shape mismatch");
+  require(c->saved_input != nullptr && m == c->m, "gat_backward: missing saved input");
+  if (c->level >= SGNN_GAT_FEATURES)
+    require(c->M.get() != nullptr, "gat_backward: cache level promises M but it is absent");
+  if (c->level == SGNN_GAT_FULL)
+    require(c->alpha.get() != nullptr && c->mask.get() != nullptr,
+            "gat_backward: cache level promises alpha/mask but they are absent");
+  require(!fg || d_input != nullptr, "gat_backward: d_input required for feature gradients");
+  (void)beta;  // the forward's beta is kept in the cache
+  if (c->dtype == SGNN_F32)
+    gat_backward_t<float>(ctx, p, (const float*)d_out, (const float*)theta,
+                          (const float*)a_src, (const float*)a_dst, c, fg != 0,
+                          (float*)d_theta, (float*)d_a_src, (float*)d_a_dst, (float*)d_bias,
+                          (float*)d_input);
+  else
+    gat_backward_t<double>(ctx, p, (const double*)d_out, (const double*)theta,
+                           (const double*)a_src, (const double*)a_dst, c, fg != 0,
+                           (double*)d_theta, (double*)d_a_src, (double*)d_a_dst,
+                           (double*)d_bias, (double*)d_input);
+  SGNN_API_END
+}
+
+int sgnn_gat_cache_destroy(sgnn_gat_cache c) {
+  SGNN_API_BEGIN
+  delete c;
+  SGNN_API_END
+}
+
+int sgnn_gat_cache_extra_bytes(sgnn_gat_cache c, int64_t* out) {
+  SGNN_API_BEGIN
+  // gat.hpp:66-71: bytes owned beyond the retained input; buffers carry +8
+  // bytes of slack for empty shapes, so report the logical sizes.
+  const int64_t sb = c->dtype == SGNN_F32 ? 4 : 8;
+  int64_t b = 0;
+  if (c->M.get()) b += sb * c->n * c->h * c->k;
+  if (c->s.get()) b += 2 * sb * c->n * c->h;
+  if (c->alpha.get()) b += (int64_t)(c->alpha.bytes() - 8) + (int64_t)(c->mask.bytes() - 8);
+  *out = b;
+  SGNN_API_END
+}
+
+int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c,
+                               const void* theta, const void* a_src, const void* a_dst,
+                               void* alpha_hq, uint8_t* mask_hq) {
+  SGNN_API_BEGIN
+  require(c && p, "gat_cache_edge_values: null argument");
+  if (c->dtype == SGNN_F32)
+    gat_edge_values_t<float>(ctx, p, c, (const float*)theta, (const float*)a_src,
+                             (const float*)a_dst, (float*)alpha_hq, mask_hq);
+  else
+    gat_edge_values_t<double>(ctx, p, c, (const double*)theta, (const double*)a_src,
+                              (const double*)a_dst, (double*)alpha_hq, mask_hq);
+  SGNN_API_END
+}
+
+int sgnn_edge_softmax(sgnn_ctx ctx, sgnn_pattern p, int32_t heads, const void* w, int dtype,
+                      void* alpha) {
+  SGNN_API_BEGIN
+  require(p && p->all_self_loops, "edge_softmax: pattern must contain all self loops");
+  const int64_t total = (int64_t)p->n * heads;
+  if (total == 0) return SGNN_OK;
+  if (dtype == SGNN_F32)
+    k_edge_softmax<float><<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
+        p->n, p->rowptr.as<int32_t>(), heads, (const float*)w, (float*)alpha);
+  else
+    k_edge_softmax<double><<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
+        p->n, p->rowptr.as<int32_t>(), heads, (const double*)w, (double*)alpha);
+  launched(ctx);
+  SGNN_API_END
+}
+
+int sgnn_sddmm(sgnn_ctx ctx, sgnn_pattern p, const void* B, int32_t f, const void* C,
+               int32_t ldc, int dtype, void* out) {
+  SGNN_API_BEGIN
+  require(p != nullptr, "sddmm: outer dimension mismatch");
+  require(ldc == p->n, "sddmm: outer dimension mismatch");
+  if (p->n == 0) return SGNN_OK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p->n, 8), 148 * 32));
+  if (dtype == SGNN_F32)
+    k_sddmm<float><<<grid, 256, 0, ctx->stream>>>(p->n, p->rowptr.as<int32_t>(),
+                                                  p->cols.as<int32_t>(), (const float*)B, f,
+                                                  (const float*)C, ldc, (float*)out);
+  else
+    k_sddmm<double><<<grid, 256, 0, ctx->stream>>>(p->n, p->rowptr.as<int32_t>(),
+                                                   p->cols.as<int32_t>(), (const double*)B, f,
+                                                   (const double*)C, ldc, (double*)out);
+  launched(ctx);
+  SGNN_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// gcn.cu -- GCN scheme engine (north-star subsystem 2; gcn.hpp:91-193).
+//
+//   transform_first          M = X Theta (tcgen05 GEMM), out = A'M + b (SpMM, bias epilogue)
+//   propagate_first[_cached] P = A'X (SpMM), out = P Theta + b (GEMM, bias epilogue);
+//                            the cached variant keeps P for backward
+//   fused_propagate          S = A'^T dX', dTheta = X^T S, dX = S Theta^T
+//   split_propagate          P = A'X, G = dX' Theta^T, dTheta = P^T dX', dX = A'^T G
+//   split_propagate_cached   as split with P from the cache (no SpMM without dX)
+// Transients come from the stream-ordered pool; A'^T products run the same
+// CSR kernel over the CSC arrays (CSR of A'^T).
+#include "common.cuh"
+#include "internal.cuh"
+
+using namespace sgnn;
+
+namespace {
+
+template <class T>
+void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* theta,
+                   const T* bias, int32_t k, const sgnn_scheme& s, T* out, sgnn_gcn_cache c) {
+  const int32_t n = A->n_rows;
+  cudaStream_t st = ctx->stream;
+  const int32_t* rp = A->rowptr.as<int32_t>();
+  const int32_t* ci = A->cols.as<int32_t>();
+  const T* av = A->vals.as<T>();
+  if (s.forward == SGNN_TRANSFORM_FIRST) {
+    DevBuf M((size_t)n * k * sizeof(T), st);
+    gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
+    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias);
+    c->saved_input = X;
+  } else {
+    DevBuf P((size_t)n * m * sizeof(T), st);
+    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr);
+    gemm<T>(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias);
+    if (s.forward == SGNN_PROPAGATE_FIRST_CACHED)
+      c->saved_propagated = std::move(P);  // reclassified into the cache (gcn.hpp:124)
+    else
+      c->saved_input = X;
+  }
+}
+
+template <class T>
+void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_t m, int32_t k,
+                    sgnn_gcn_cache c, bool fg, T* d_theta, T* d_bias, T* d_input) {
+  const int32_t n = A->n_rows;
+  cudaStream_t st = ctx->stream;
+  const int32_t* rp = A->rowptr.as<int32_t>();
+  const int32_t* ci = A->cols.as<int32_t>();
+  const T* av = A->vals.as<T>();
+  const int32_t* cp = A->colptr.as<int32_t>();
+  const int32_t* cr = A->crows.as<int32_t>();
+  const T* cv = A->cvals.as<T>();
+  column_sums<T>(ctx, G, n, k, d_bias);
+  switch (c->scheme.backward) {
+    case SGNN_FUSED_PROPAGATE: {
+      const T* X = static_cast<const T*>(c->saved_input);
+      DevBuf S((size_t)n * k * sizeof(T), st);
+      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr);
+      gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
+      if (fg) gemm<T>(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input);
+      break;
+    }
+    case SGNN_SPLIT_PROPAGATE: {
+      const T* X = static_cast<const T*>(c->saved_input);
+      DevBuf P((size_t)n * m * sizeof(T), st);
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr);
+      gemm<T>(ctx, P.as<T>(), n, m, G, n, k, true, false, d_theta);
+      if (fg) {
+        DevBuf G2((size_t)n * m * sizeof(T), st);
+        gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr);
+      }
+      break;
+    }
+    case SGNN_SPLIT_PROPAGATE_CACHED: {
+      const T* P = c->saved_propagated.as<T>();
+      gemm<T>(ctx, P, n, m, G, n, k, true, false, d_theta);
+      if (fg) {
+        DevBuf G2((size_t)n * m * sizeof(T), st);
+        gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr);
+      }
+      break;
+    }
+    default: throw invalid_argument("gcn_backward: unknown scheme");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgnn_gcn_forward(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m, const void* theta,
+                     const void* bias, int32_t k, const sgnn_scheme* scheme, void* out,
+                     sgnn_gcn_cache* cache) {
+  SGNN_API_BEGIN
+  require(A && scheme && cache, "gcn_forward: null argument");
+  require(A->n_rows == A->n_cols, "gcn_forward: adjacency/input shape mismatch");
+  require(m >= 1 && k >= 1, "gcn_forward: input width does not match theta");
+  require(scheme->forward >= 0 && scheme->forward <= 2 && scheme->backward >= 0 &&
+              scheme->backward <= 2,
+          "gcn_forward: unknown scheme");
+  auto* c = new sgnn_gcn_cache_s;
+  c->scheme = *scheme;
+  c->dtype = A->dtype;
+  c->n = A->n_rows;
+  c->m = m;
+  c->saved_propagated.set_stream(ctx->stream);
+  try {
+    if (A->dtype == SGNN_F32)
+      gcn_forward_t<float>(ctx, A, (const float*)X, m, (const float*)theta, (const float*)bias,
+                           k, *scheme, (float*)out, c);
+    else
+      gcn_forward_t<double>(ctx, A, (const double*)X, m, (const double*)theta,
+                            (const double*)bias, k, *scheme, (double*)out, c);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *cache = c;
+  SGNN_API_END
+}
+
+int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* theta, int32_t m,
+                      int32_t k, sgnn_gcn_cache c, int fg, void* d_theta, void* d_bias,
+                      void* d_input) {
+  SGNN_API_BEGIN
+  require(c != nullptr, "gcn_backward: missing saved input");
+  require(!c->consumed, "gcn_backward: cache already consumed");
+  c->consumed = true;  // gcn.hpp:137-138: consumed before any other validation
+  require(A && c->m == m, "gcn_backward: gradient shape mismatch");
+  const bool cached = c->scheme.backward == SGNN_SPLIT_PROPAGATE_CACHED;
+  if (cached)
+    require(c->saved_propagated.get() != nullptr,
+            "gcn_backward: cached scheme without saved A'X");
+  else
+    require(c->saved_input != nullptr, "gcn_backward: missing saved input");
+  require(!fg || d_input != nullptr, "gcn_backward: d_input required for feature gradients");
+  if (A->dtype == SGNN_F32)
+    gcn_backward_t<float>(ctx, A, (const float*)d_out, (const float*)theta, m, k, c, fg != 0,
+                          (float*)d_theta, (float*)d_bias, (float*)d_input);
+  else
+    gcn_backward_t<double>(ctx, A, (const double*)d_out, (const double*)theta, m, k, c, fg != 0,
+                           (double*)d_theta, (double*)d_bias, (double*)d_input);
+  // the cached P is released once consumed (its lifetime ends with backward)
+  c->saved_propagated.reset();
+  SGNN_API_END
+}
+
+int sgnn_gcn_cache_destroy(sgnn_gcn_cache c) {
+  SGNN_API_BEGIN
+  delete c;
+  SGNN_API_END
+}
+
+int sgnn_gcn_cache_retained_bytes(sgnn_gcn_cache c, int64_t* out) {
+  SGNN_API_BEGIN
+  const int64_t sb = c->dtype == SGNN_F32 ? 4 : 8;
+  *out = c->saved_propagated.get() ? (int64_t)c->saved_propagated.bytes()
+                                   : (c->saved_input ? sb * c->n * c->m : 0);
+  SGNN_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// internal.cuh -- device-side object layouts and the kernel launchers shared
+// between translation units of libsgnn_cuda.so.
+#pragma once
+
+#include "common.cuh"
+
+// AdjacencyOp (kernels.hpp:191-211): forward CSR and the CSC arrays that are
+// the CSR of A^T (zero-copy transpose of sparse.hpp:400-420), owned here.
+struct sgnn_adj_s {
+  int32_t n_rows = 0, n_cols = 0;
+  int64_t nnz = 0;
+  int dtype = SGNN_F32;
+  int format = SGNN_CSC;
+  sgnn::DevBuf rowptr, cols, vals;    // CSR of A
+  sgnn::DevBuf colptr, crows, cvals;  // CSC of A == CSR of A^T
+  ~sgnn_adj_s();
+};
+
+// SparsePattern (pattern.hpp:17-95)
+struct sgnn_pattern_s {
+  int32_t n = 0;
+  int64_t nnz = 0;
+  bool all_self_loops = false;
+  sgnn::DevBuf rowptr, cols, colptr, rows, perm, diag;
+  ~sgnn_pattern_s();
+};
+
+// GcnCache (gcn.hpp:66-76): exactly one of the borrowed X / owned P
+struct sgnn_gcn_cache_s {
+  sgnn_scheme scheme{};
+  int dtype = SGNN_F32;
+  int32_t n = 0, m = 0;
+  const void* saved_input = nullptr;  // borrowed (aliases the caller's X)
+  sgnn::DevBuf saved_propagated;      // owned P = A'X
+  bool consumed = false;
+};
+
+// GatCache (gat.hpp:56-72); edge values edge-major q x h
+struct sgnn_gat_cache_s {
+  int level = SGNN_GAT_NONE;
+  int dtype = SGNN_F32;
+  int32_t n = 0, m = 0, h = 0, k = 0;
+  double beta = 0.2;
+  const void* saved_input = nullptr;  // borrowed, always retained
+  sgnn::DevBuf M;                     // level >= features
+  sgnn::DevBuf s, d;                  // level == node_attention
+  sgnn::DevBuf alpha, mask;           // level == full
+  bool consumed = false;
+};
+
+namespace sgnn {
+
+void build_ptr(sgnn_ctx ctx, const int32_t* sorted_ids, int64_t nnz, int32_t n, int32_t* ptr);
+
+// C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
+template <class T>
+void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
+              const T* vals, const T* B, int32_t f, T* C, const T* bias);
+
+// C = op(A) op(B) (row-major); A ra x ca, B rb x cb; bias added per column of C
+template <class T>
+void gemm(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int32_t rb, int32_t cb,
+          bool ta, bool tb, T* C, const T* bias = nullptr);
+
+template <class T>
+void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out);
+
+template <class T>
+void random_uniform(sgnn_ctx ctx, int64_t count, uint64_t seed, double lo, double hi, T* out);
+
+}  // namespace sgnn
