@@ -1,0 +1,355 @@
+"""Benchmark: GCN layer forward+backward on the OGB-Arxiv-shaped synthetic graph.
+
+Metric (BASELINE.json): "GCN/GAT layer fwd+bwd ms on OGB-Arxiv shape; SpMM/SDDMM
+HBM GB/s vs peak".  Headline workload (configs[1]): one GCN layer, 128 -> 256
+features, input-feature gradients on, adaptive scheme with caching (the
+reference resolves it to propagate_first_cached + split_propagate_cached),
+graph = synthetic_graph(169343, 1166243/169343, seed=1) -> gcn_normalize
+(q' = 1,335,587).  Inputs follow the reference harness seeds (bench.hpp:182-194):
+X from seed+11, dX' from seed+12, parameters from seed+13, all generated on the
+device with the reference's counter-based RNG (bit-identical values).
+
+  value        device time per fwd+bwd step, inputs resident in HBM, L2 flushed
+               (256 MiB write) before every timed step, CUDA events on the stream
+  e2e          the same step through the public API with HOST buffers: pinned
+               H2D of X and dX', D2H of out, dTheta, db, dX inside the timed region
+  roofline     dominant kernel of the step, timed live here in isolation
+  cpu_baseline the reference itself (oracle/_ref, compiled from the unmodified
+               headers, OpenMP on every host core) on the same workload
+
+`--impl reference` times the reference's CPU implementation of the same
+workload on the host (rank 0 only under torchrun) and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ARXIV_N = 169343
+ARXIV_EDGES = 1166243
+SEED = 1
+M_IN, K_OUT = 128, 256
+GAT_H, GAT_K = 8, 32
+METRIC = "GCN/GAT layer fwd+bwd ms on OGB-Arxiv shape; SpMM/SDDMM HBM GB/s vs peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the reference's own OpenMP CPU path
+# ---------------------------------------------------------------------------
+def reference_cpu(steps, warmup, kind=0, cores=None):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy  # reference compiled from its unmodified headers (oracle/_ref)
+
+    if not refpy.available():
+        raise RuntimeError("oracle/_ref/libsgnn_ref.so missing (build() in the dev container)")
+    L = refpy.load()
+    if cores:
+        L.ref_set_num_threads(cores)
+    used = L.ref_num_threads()
+    t0 = time.perf_counter()
+    if kind == 0:
+        h = L.ref_bench_create(0, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, K_OUT, 1, 1, 0, 1, 0,
+                               2)
+    else:
+        h = L.ref_bench_create(1, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GAT_K, GAT_H, 1, 0,
+                               0, 3, 1)
+    if not h:
+        raise RuntimeError(L.ref_last_error().decode())
+    setup_s = time.perf_counter() - t0
+    for _ in range(warmup):
+        L.ref_bench_step(h)
+    times = [L.ref_bench_step(h) for _ in range(steps)]
+    L.ref_bench_destroy(h)
+    return {"ms": 1e3 * statistics.median(times), "cores": used, "setup_s": setup_s,
+            "steps": steps, "warmup": warmup}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    r = reference_cpu(args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config(),
+        "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": r["cores"],
+                         "kind": "reference",
+                         "sample": f"{args.steps} full fwd+bwd steps of the workload (median) "
+                                   f"after {args.warmup} warmups; reference headers -O3 "
+                                   "-fopenmp, S=float, CSC"},
+        "e2e": {"value": round(r["ms"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config():
+    return {"workload": "gcn_layer_fwd_bwd arxiv-shaped 128->256 fg=1 adaptive+caching",
+            "graph": f"synthetic_graph(n={ARXIV_N}, deg={ARXIV_EDGES}/{ARXIV_N}, seed={SEED})"
+                     " + gcn_normalize",
+            "n": ARXIV_N, "m": M_IN, "k": K_OUT, "needs_feature_grad": True,
+            "scheme_policy": "adaptive", "caching": True, "format": "csc",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2308_12093_b200 import device as d
+
+    ctx = d.Context.default(local)
+    dev = ctx.device
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- workload (preprocessing outside timing, like bench.hpp:193-219) ----
+    t0 = time.perf_counter()
+    src, dst = d.synthetic_graph(ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED)
+    A = d.Adjacency.gcn_operator(ARXIV_N, src, dst, torch.float32, "csc", ctx)
+    P = d.Pattern.gat_pattern(ARXIV_N, src, dst, ctx)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    n, q = ARXIV_N, A.nnz
+    X = d.random_uniform(n, M_IN, SEED + 11, ctx=ctx)
+    G = d.random_uniform(n, K_OUT, SEED + 12, ctx=ctx)
+    theta, bias = d.gcn_params(M_IN, K_OUT, SEED + 13, ctx=ctx)
+    scheme = d.resolve_scheme("adaptive", M_IN, K_OUT, True, True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        out, cache = d.gcn_forward(A, X, theta, bias, scheme)
+        return (out,) + d.gcn_backward(A, G, theta, cache, True)
+
+    def timed(fn, iters, warm):
+        for _ in range(warm):
+            fn()
+        ms = []
+        for _ in range(iters):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return ms
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ctx.launch_count
+    with Clocks(local) as clk:
+        step_ms = timed(step, args.steps, 0)
+    launches = (ctx.launch_count - launches0) // max(1, args.steps)
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- component breakdown + roofline (isolated launches, same stream) ----
+    hbm, bf16, peak_kind = _peaks()
+    Pm = torch.empty((n, M_IN), dtype=torch.float32, device=dev)
+    comps = {}
+    reps = max(3, args.steps)
+    comps["spmm_fwd_f128"] = statistics.mean(timed(lambda: A.spmm(X, out=Pm), reps, 2))
+    comps["gemm_PxTheta"] = statistics.mean(timed(lambda: d.gemm(Pm, theta), reps, 2))
+    comps["gemm_PtG"] = statistics.mean(timed(lambda: d.gemm(Pm, G, True, False), reps, 2))
+    comps["gemm_GThetaT"] = statistics.mean(timed(lambda: d.gemm(G, theta, False, True), reps, 2))
+    G2 = d.gemm(G, theta, False, True)
+    comps["spmm_bwd_f128"] = statistics.mean(timed(lambda: A.spmm(G2, transposed=True, out=Pm),
+                                                   reps, 2))
+    comps["colsum_db"] = statistics.mean(timed(lambda: d.column_sums(G), reps, 2))
+    # algorithmic bytes per launch: CSR SpMM f: 4(n+1)+8q'+8nf
+    spmm_bytes = 4 * (n + 1) + 8 * q + 8 * n * M_IN
+    gemm_bytes = {"gemm_PxTheta": 4 * (n * M_IN + M_IN * K_OUT + n * K_OUT),
+                  "gemm_PtG": 4 * (n * M_IN + n * K_OUT + M_IN * K_OUT),
+                  "gemm_GThetaT": 4 * (n * K_OUT + M_IN * K_OUT + n * M_IN)}
+    dominant = max(comps, key=comps.get)
+    dom_bytes = spmm_bytes if dominant.startswith("spmm") else (
+        gemm_bytes.get(dominant, 4 * n * K_OUT))
+    achieved = dom_bytes / (comps[dominant] * 1e-3) / 1e9
+    spmm_gbs = spmm_bytes / (comps["spmm_fwd_f128"] * 1e-3) / 1e9
+    roofline = {"kernel": dominant, "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "traffic": None, "algorithmic_bytes": dom_bytes, "peak_source": peak_kind,
+                "ms": round(comps[dominant], 4)}
+
+    # ---- GAT layer (h=8, k=32, cache level full) on the same graph ----------
+    Xg = X
+    th_g, as_g, ad_g, b_g = d.gat_params(M_IN, GAT_H, GAT_K, SEED + 13, ctx=ctx)
+    Gg = d.random_uniform(n, GAT_H * GAT_K, SEED + 12, ctx=ctx)
+
+    def gat_step():
+        out, cache = d.gat_forward(P, Xg, th_g, as_g, ad_g, b_g, GAT_H, 0.2, "full")
+        return d.gat_backward(P, Gg, th_g, as_g, ad_g, cache, True)
+
+    gat_ms = statistics.mean(timed(gat_step, max(3, args.steps), 2))
+
+    # ---- e2e through the public API with host buffers -----------------------
+    hX = torch.empty((n, M_IN), dtype=torch.float32, pin_memory=True)
+    hG = torch.empty((n, K_OUT), dtype=torch.float32, pin_memory=True)
+    hX.copy_(X)
+    hG.copy_(G)
+    h_out = torch.empty((n, K_OUT), dtype=torch.float32, pin_memory=True)
+    h_dth = torch.empty((M_IN, K_OUT), dtype=torch.float32, pin_memory=True)
+    h_db = torch.empty(K_OUT, dtype=torch.float32, pin_memory=True)
+    h_dx = torch.empty((n, M_IN), dtype=torch.float32, pin_memory=True)
+
+    def e2e_step():
+        Xd = hX.to(dev, non_blocking=True)
+        Gd = hG.to(dev, non_blocking=True)
+        out, cache = d.gcn_forward(A, Xd, theta, bias, scheme)
+        dth, db, dx = d.gcn_backward(A, Gd, theta, cache, True)
+        h_out.copy_(out, non_blocking=True)
+        h_dth.copy_(dth, non_blocking=True)
+        h_db.copy_(db, non_blocking=True)
+        h_dx.copy_(dx, non_blocking=True)
+
+    e2e_ms = statistics.mean(timed(e2e_step, max(3, args.steps), 2))
+    h2d = hX.numel() * 4 + hG.numel() * 4
+    d2h = (h_out.numel() + h_dth.numel() + h_db.numel() + h_dx.numel()) * 4
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            r = reference_cpu(args.cpu_steps, 1)
+            cpu = {"value": round(r["ms"], 2), "unit": "ms", "cores": r["cores"],
+                   "kind": "reference",
+                   "sample": f"{args.cpu_steps} full fwd+bwd steps of the same workload "
+                             "(median, 1 warmup), reference headers -O3 -fopenmp, S=float, CSC"}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generators, device-side)",
+        "config": dict(_config(), scheme=str(scheme), nnz=q),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "edges_per_s": round(q / (ms * 1e-3), 1),
+        "spmm_gbs": round(spmm_gbs, 1),
+        "breakdown_ms": {k: round(v, 4) for k, v in comps.items()},
+        "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K, "level": "full",
+                      "nnz": P.nnz},
+        "setup_s": round(setup_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -93,7 +93,7 @@ typedef struct sgnn_gat_cache_s* sgnn_gat_cache;
 /* common.hpp:37-43 require() message of the last failing call on this thread */
 const char* sgnn_last_error(void);
 const char* sgnn_version(void);
-/* stream: a cudaStream_t (NULL = create an owned non-blocking stream) */
+/* stream: a cudaStream_t; NULL = the default stream (CUDA convention) */
 int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out);
 int sgnn_ctx_destroy(sgnn_ctx ctx);
 int sgnn_ctx_set_stream(sgnn_ctx ctx, void* stream);

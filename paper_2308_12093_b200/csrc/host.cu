@@ -27,12 +27,9 @@ int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out) {
   c->device = device;
   SGNN_CUDA(cudaSetDevice(device));
   SGNN_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-  if (stream) {
-    c->stream = static_cast<cudaStream_t>(stream);
-  } else {
-    SGNN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    c->own_stream = true;
-  }
+  // NULL is CUDA's default stream (torch's default stream reports handle 0),
+  // so work stays ordered with the caller's allocations and copies.
+  c->stream = static_cast<cudaStream_t>(stream);
   // Keep freed transients pooled: the stream-ordered allocator then never
   // returns memory to the driver between layer calls.
   cudaMemPool_t pool;
@@ -56,7 +53,7 @@ int sgnn_ctx_destroy(sgnn_ctx ctx) {
 
 int sgnn_ctx_set_stream(sgnn_ctx ctx, void* stream) {
   SGNN_API_BEGIN
-  require(ctx && stream, "sgnn_ctx_set_stream: null argument");
+  require(ctx != nullptr, "sgnn_ctx_set_stream: null context");
   if (ctx->own_stream) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
