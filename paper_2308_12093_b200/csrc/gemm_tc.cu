@@ -1,12 +1,455 @@
-// gemm_tc.cu -- tcgen05 (5th-gen tensor core) GEMM for the float32 dense
-// transforms X.Theta and their gradients.  Placeholder until the kernel lands:
-// returns false so dense.cu falls back to the SIMT kernel.
+// gemm_tc.cu -- tcgen05 (5th-generation tensor core) GEMM for the float32
+// dense transforms of the path: X.Theta / P.Theta (forward), X^T S / P^T dX'
+// (dTheta, split-K over the n-long reduction) and S.Theta^T / dX'.Theta^T (dX).
+//
+// Accuracy: the north star requires fp32 results within 1e-4 of the float64
+// reference; plain TF32 misses that.  Each fp32 operand tile is
+// split in shared memory into hi = tf32(x) (low 13 mantissa bits cleared) and
+// lo = x - hi, and the tile product is hi.hi + hi.lo + lo.hi ("3xTF32"),
+// accumulated in fp32 in TMEM -- ~2^-21 relative error per product.
+//
+// Structure (one 128 x BN output tile per CTA, K pipelined in BK=32 stages):
+//   warp 0      TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier tx)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
+//               M=128, N=BN, K=8), tcgen05.commit frees smem stages
+//   warps 2..5  split converters (raw -> hi in place, lo to a twin buffer,
+//               fence.proxy.async) during the main loop, then the epilogue
+//               (tcgen05.ld 32x32b.x32 -> registers -> +bias -> global)
+// Operands may be K-major or MN-major (UMMA transpose bits), so X^T . S reads
+// X and S in place -- no transposed copies.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
 #include "internal.cuh"
 
 namespace sgnn {
-bool gemm_tc_f32(sgnn_ctx, const float*, int32_t, int32_t, const float*, int32_t, int32_t, bool,
-                 bool, float*, const float*) {
-  return false;
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int NUM_THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, M=128, N=n, majors
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4)                      // c_format F32
+         | (2u << 7)                    // a_format TF32
+         | (2u << 10)                   // b_format TF32
+         | ((a_mn ? 1u : 0u) << 15)     // a_major
+         | ((b_mn ? 1u : 0u) << 16)     // b_major
+         | ((uint32_t)(n >> 3) << 17)   // N >> 3
+         | ((uint32_t)(BM >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Split a raw fp32 tile in place into hi (tf32-exact) and write lo.
+__device__ __forceinline__ void split_tile(float4* raw, float4* lo, int n4, int tid, int nthr) {
+  for (int i = tid; i < n4; i += nthr) {
+    float4 v = raw[i];
+    float4 h, l;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    l.x = __fsub_rn(v.x, h.x);
+    l.y = __fsub_rn(v.y, h.y);
+    l.z = __fsub_rn(v.z, h.z);
+    l.w = __fsub_rn(v.w, h.w);
+    raw[i] = h;
+    lo[i] = l;
+  }
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES >= 4 ? 4 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// C[M x N] (+bias) = op(A) op(B); or partial[z] when `part` != nullptr.
+template <bool A_MN, bool B_MN, int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              int M, int N, int K, int kchunk, float* __restrict__ C, int ldc,
+              const float* __restrict__ bias, float* __restrict__ part) {
+  using CF = Cfg<BN>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
+  uint64_t* conv = full + S;
+  uint64_t* empty = conv + S;
+  uint64_t* accum = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int k_begin = blockIdx.z * kchunk;
+  const int k_end = min(K, k_begin + kchunk);
+  const int nk = (k_end - k_begin + BK - 1) / BK;
+
+  auto a_raw = [&](int s) { return smem + s * CF::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + CF::A_BYTES; };
+  auto b_raw = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES + CF::B_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % S;
+        const uint32_t ph = (ks / S) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+        const int kc = k_begin + ks * BK;
+        if (A_MN) {  // A stored K x M: boxes of 32 M-elements x 32 K-rows
+#pragma unroll
+          for (int b = 0; b < BM / 32; ++b)
+            tma_load_2d(a_raw(s) + b * 4096, &tmA, &full[s], m0 + 32 * b, kc);
+        } else {  // A stored M x K: one box of 32 K x 128 rows
+          tma_load_2d(a_raw(s), &tmA, &full[s], kc, m0);
+        }
+        if (B_MN) {  // B stored K x N
+#pragma unroll
+          for (int b = 0; b < BN / 32; ++b)
+            tma_load_2d(b_raw(s) + b * 4096, &tmB, &full[s], n0 + 32 * b, kc);
+        } else {  // B stored N x K
+          tma_load_2d(b_raw(s), &tmB, &full[s], kc, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % S;
+        const uint32_t ph = (ks / S) & 1;
+        mbar_wait(&conv[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ah = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
+        const uint32_t bh = smem_u32(b_raw(s)), bl = smem_u32(b_lo(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          // K-major: advance 32 B inside the swizzled 128 B row (LBO unused = 16 B,
+          // SBO = 1024 B between 8-row groups).  MN-major: next 8-row K group
+          // (1024 B); LBO = 4096 B between 32-element MN atoms.
+          const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+          const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+          const uint32_t alb = A_MN ? 4096 : 16, asb = 1024;
+          const uint32_t blb = B_MN ? 4096 : 16, bsb = 1024;
+          const uint64_t dah = smem_desc(ah + aoff, alb, asb);
+          const uint64_t dal = smem_desc(al + aoff, alb, asb);
+          const uint64_t dbh = smem_desc(bh + boff, blb, bsb);
+          const uint64_t dbl = smem_desc(bl + boff, blb, bsb);
+          const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem, dah, dbh, idesc, acc);
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+          mma_tf32(tmem, dal, dbh, idesc, 1u);
+        }
+        umma_commit(&empty[s]);  // stage s free once these MMAs retire
+      }
+      umma_commit(accum);
+    }
+  } else {
+    // ---------------- split converters, then epilogue ----------------
+    const int ctid = threadIdx.x - 64;  // 0..127
+    for (int ks = 0; ks < nk; ++ks) {
+      const int s = ks % S;
+      const uint32_t ph = (ks / S) & 1;
+      mbar_wait(&full[s], ph);
+      split_tile(reinterpret_cast<float4*>(a_raw(s)), reinterpret_cast<float4*>(a_lo(s)),
+                 CF::A_BYTES / 16, ctid, 128);
+      split_tile(reinterpret_cast<float4*>(b_raw(s)), reinterpret_cast<float4*>(b_lo(s)),
+                 CF::B_BYTES / 16, ctid, 128);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+    }
+    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (one output row per thread)
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    const bool vec = ((ldc & 3) == 0) && ((N & 3) == 0);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+      if (row >= M) continue;
+      const int col0 = n0 + c;
+      if (part) {
+        float* dst = part + ((int64_t)blockIdx.z * M + row) * N;
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) dst[col0 + j] = __uint_as_float(r[j]);
+      } else {
+        float* dst = C + (int64_t)row * ldc;
+        if (vec && col0 + 32 <= N) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+            if (bias) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0 + j));
+              v.x = __fadd_rn(v.x, b.x);
+              v.y = __fadd_rn(v.y, b.y);
+              v.z = __fadd_rn(v.z, b.z);
+              v.w = __fadd_rn(v.w, b.w);
+            }
+            *reinterpret_cast<float4*>(dst + col0 + j) = v;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < N)
+              dst[col0 + j] = bias ? __fadd_rn(__uint_as_float(r[j]), bias[col0 + j])
+                                   : __uint_as_float(r[j]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)BN));
+  }
+}
+
+__global__ void k_reduce_splits(int splits, int64_t MN, int N, const float* __restrict__ part,
+                                float* __restrict__ C, int ldc, const float* __restrict__ bias) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < MN;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += (double)part[(int64_t)z * MN + x];
+    const int64_t row = x / N, col = x % N;
+    float v = (float)s;
+    if (bias) v = __fadd_rn(v, bias[col]);
+    C[row * ldc + col] = v;
+  }
+}
+
+// ---- host side -------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map over a row-major [outer][inner] array with leading
+// dimension ld (elements), box {32, box_outer}, 128-byte swizzle, OOB -> 0
+static bool make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld,
+                     int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
+                   int K, int splits, int kchunk, float* C, const float* bias, float* part) {
+  auto kern = k_gemm_tc<A_MN, B_MN, BN>;
+  const int smem = Cfg<BN>::SMEM;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    SGNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
+  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, C, N, bias, part);
+  launched(ctx);
+}
+
+template <int BN>
+static void dispatch_major(sgnn_ctx ctx, bool a_mn, bool b_mn, const CUtensorMap& ma,
+                           const CUtensorMap& mb, int M, int N, int K, int splits, int kchunk,
+                           float* C, const float* bias, float* part) {
+  if (a_mn && b_mn) launch<true, true, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
+  else if (a_mn) launch<true, false, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
+  else if (b_mn) launch<false, true, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
+  else launch<false, false, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
+}
+
+}  // namespace tc
+
+static bool tc_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SGNN_DISABLE_TCGEN05");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Returns false (caller falls back to the SIMT kernel) when the shape or the
+// operand alignment does not fit the TMA/UMMA path.
+bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias) {
+  using namespace tc;
+  if (tc_disabled()) return false;
+  const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
+  if (M <= 0 || N <= 0 || K <= 0) return false;
+  if ((int64_t)M * N * K < (int64_t)1 << 20) return false;  // tiny: SIMT is fine
+  if ((ca & 3) || (cb & 3)) return false;                     // 16-byte row pitch for TMA
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
+  if ((reinterpret_cast<uintptr_t>(C) & 15) || (bias && (reinterpret_cast<uintptr_t>(bias) & 15)))
+    return false;
+  const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
+  CUtensorMap ma, mb;
+  const bool a_mn = ta, b_mn = !tb;
+  // A: ta -> stored K x M (MN-major), else M x K (K-major)
+  const bool okA = a_mn ? make_map(&ma, A, M, K, ca, BK) : make_map(&ma, A, K, M, ca, BM);
+  // B: tb -> stored N x K (K-major), else K x N (MN-major)
+  const bool okB = b_mn ? make_map(&mb, B, N, K, cb, BK) : make_map(&mb, B, K, N, cb, BN);
+  if (!okA || !okB) return false;
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
+  int splits = 1;
+  const int ksteps = (int)ceil_div(K, BK);
+  if (tiles < ctx->num_sms && ksteps >= 16) {
+    splits = (int)std::min<int64_t>(ceil_div(ctx->num_sms, tiles), ksteps / 8);
+    if (splits < 1) splits = 1;
+  }
+  const int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
+  splits = (int)ceil_div(K, kchunk);
+  DevBuf part;
+  float* pp = nullptr;
+  if (splits > 1) {
+    part = DevBuf((size_t)splits * M * N * sizeof(float), ctx->stream);
+    pp = part.as<float>();
+  }
+  switch (BN) {
+    case 32: dispatch_major<32>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
+    case 64: dispatch_major<64>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
+    default: dispatch_major<128>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
+  }
+  if (splits > 1) {
+    const int64_t MN = (int64_t)M * N;
+    k_reduce_splits<<<grid_for(ctx, MN, 256), 256, 0, ctx->stream>>>(splits, MN, N, pp, C, N,
+                                                                     bias);
+    launched(ctx);
+  }
+  return true;
+}
+
 }  // namespace sgnn

@@ -35,7 +35,7 @@ class _CudaArray:
 
     def __init__(self, ptr, n, typestr):
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
-                                         "data": (int(ptr or 0), True), "version": 3,
+                                         "data": (int(ptr or 0), False), "version": 3,
                                          "strides": None}
 
 
@@ -71,6 +71,13 @@ class Context:
             with torch.cuda.device(idx):
                 ctx = cls._default[idx] = cls(idx)
         return ctx
+
+    def set_stream(self, stream):
+        """Enqueue subsequent work on `stream` (a torch.cuda.Stream), e.g. the
+        capture stream of torch.cuda.graph: layer calls contain no host
+        synchronisation, so a whole fwd+bwd step can be captured and replayed."""
+        check(lib.sgnn_ctx_set_stream(self.handle, C.c_void_p(stream.cuda_stream)))
+        self.stream = stream
 
     @property
     def launch_count(self):
