@@ -70,14 +70,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, version 1.  Layout type 2 = SWIZZLE_128B
+// (16-byte chunks, K-major tiles); 1 = SWIZZLE_128B_BASE32B (32-byte chunks,
+// 4-row period) -- the only layout UMMA accepts for MN-major tf32 operands.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // version (sm100)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -237,17 +240,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t bh = smem_u32(b_raw(s)), bl = smem_u32(b_lo(s));
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          // K-major: advance 32 B inside the swizzled 128 B row (LBO unused = 16 B,
-          // SBO = 1024 B between 8-row groups).  MN-major: next 8-row K group
-          // (1024 B); LBO = 4096 B between 32-element MN atoms.
+          // K-major (SW128): advance 32 B inside the swizzled 128 B row; LBO
+          // unused (16 B), SBO = 1024 B between 8-row groups.
+          // MN-major (SW128_BASE32B): next 8 K-rows = 1024 B; LBO = 4096 B
+          // between 32-element MN atoms, SBO = 512 B between 4-row K groups.
           const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
           const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-          const uint32_t alb = A_MN ? 4096 : 16, asb = 1024;
-          const uint32_t blb = B_MN ? 4096 : 16, bsb = 1024;
-          const uint64_t dah = smem_desc(ah + aoff, alb, asb);
-          const uint64_t dal = smem_desc(al + aoff, alb, asb);
-          const uint64_t dbh = smem_desc(bh + boff, blb, bsb);
-          const uint64_t dbl = smem_desc(bl + boff, blb, bsb);
+          const uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
+          const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
+          const uint64_t dah = smem_desc(ah + aoff, alb, asb, alt);
+          const uint64_t dal = smem_desc(al + aoff, alb, asb, alt);
+          const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
+          const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
           const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
           mma_tf32(tmem, dah, dbh, idesc, acc);
           mma_tf32(tmem, dah, dbl, idesc, 1u);
@@ -353,7 +357,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2-D fp32 tensor map over a row-major [outer][inner] array with leading
 // dimension ld (elements), box {32, box_outer}, 128-byte swizzle, OOB -> 0
 static bool make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t ld,
-                     int box_outer) {
+                     int box_outer, bool mn_major) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -361,7 +365,8 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t o
   cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -419,9 +424,9 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   CUtensorMap ma, mb;
   const bool a_mn = ta, b_mn = !tb;
   // A: ta -> stored K x M (MN-major), else M x K (K-major)
-  const bool okA = a_mn ? make_map(&ma, A, M, K, ca, BK) : make_map(&ma, A, K, M, ca, BM);
+  const bool okA = a_mn ? make_map(&ma, A, M, K, ca, BK, true) : make_map(&ma, A, K, M, ca, BM, false);
   // B: tb -> stored N x K (K-major), else K x N (MN-major)
-  const bool okB = b_mn ? make_map(&mb, B, N, K, cb, BK) : make_map(&mb, B, K, N, cb, BN);
+  const bool okB = b_mn ? make_map(&mb, B, N, K, cb, BK, true) : make_map(&mb, B, K, N, cb, BN, false);
   if (!okA || !okB) return false;
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
   int splits = 1;
