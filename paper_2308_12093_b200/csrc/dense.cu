@@ -172,45 +172,67 @@ void gemm<double>(sgnn_ctx ctx, const double* A, int32_t ra, int32_t ca, const d
 }
 
 // ---------------------------------------------------------------------------
-// column_sums (dense.hpp:272-282): row chunks accumulate in float64, chunk
-// partials are combined in chunk order -- deterministic, ~exact.
+// column_sums (dense.hpp:272-282): blocks own contiguous row chunks and
+// accumulate in float64 (coalesced row reads); the chunk partials are then
+// combined by a fixed-shape tree -- deterministic, ~exact, HBM-bound.
 // ---------------------------------------------------------------------------
 template <class T>
-__global__ void k_colsum_partial(const T* __restrict__ X, int32_t rows, int32_t cols,
-                                 int32_t chunk, double* __restrict__ part) {
-  const int32_t r0 = blockIdx.y * chunk;
+__global__ void __launch_bounds__(256) k_colsum_partial(const T* __restrict__ X, int32_t rows,
+                                                        int32_t cols, int32_t chunk,
+                                                        double* __restrict__ part) {
+  const int32_t r0 = blockIdx.x * chunk;
   const int32_t r1 = min(rows, r0 + chunk);
-  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int32_t i = r0; i < r1; ++i) s += (double)X[(int64_t)i * cols + j];
-    part[(int64_t)blockIdx.y * cols + j] = s;
+  for (int32_t j = threadIdx.x; j < cols; j += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int32_t i = r0;
+    for (; i + 3 < r1; i += 4) {
+      s0 += (double)X[(int64_t)i * cols + j];
+      s1 += (double)X[(int64_t)(i + 1) * cols + j];
+      s2 += (double)X[(int64_t)(i + 2) * cols + j];
+      s3 += (double)X[(int64_t)(i + 3) * cols + j];
+    }
+    for (; i < r1; ++i) s0 += (double)X[(int64_t)i * cols + j];
+    part[(int64_t)blockIdx.x * cols + j] = (s0 + s1) + (s2 + s3);
   }
 }
 
+// out[j] = sum over nchunks partials; 8 warps split the chunk list, lanes own
+// columns, smem combine in warp order.
 template <class T>
-__global__ void k_colsum_final(int32_t nchunks, int32_t cols, const double* __restrict__ part,
-                               T* __restrict__ out) {
-  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int32_t c = 0; c < nchunks; ++c) s += part[(int64_t)c * cols + j];
-    out[j] = (T)s;
+__global__ void __launch_bounds__(256) k_colsum_final(int32_t nchunks, int32_t cols,
+                                                      const double* __restrict__ part,
+                                                      T* __restrict__ out) {
+  __shared__ double sh[8][33];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t j = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (j < cols)
+    for (int32_t c = w; c < nchunks; c += 8) s += part[(int64_t)c * cols + j];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && j < cols) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+    out[j] = (T)t;
   }
 }
 
 template <class T>
 void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out) {
   if (cols == 0) return;
-  const int32_t chunk = 256;
+  const int32_t target = ctx->num_sms * 4;
+  int32_t chunk = rows > 0 ? (int32_t)ceil_div(rows, target) : 1;
+  if (chunk < 16) chunk = 16;
   const int32_t nchunks = rows > 0 ? (int32_t)ceil_div(rows, chunk) : 1;
   DevBuf part((size_t)nchunks * cols * sizeof(double), ctx->stream);
-  dim3 g((unsigned)ceil_div(cols, 128), (unsigned)nchunks);
   if (rows == 0) {
     SGNN_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), ctx->stream));
   } else {
-    k_colsum_partial<T><<<g, 128, 0, ctx->stream>>>(X, rows, cols, chunk, part.as<double>());
+    k_colsum_partial<T><<<nchunks, 256, 0, ctx->stream>>>(X, rows, cols, chunk,
+                                                          part.as<double>());
     launched(ctx);
   }
-  k_colsum_final<T><<<(unsigned)ceil_div(cols, 128), 128, 0, ctx->stream>>>(
+  k_colsum_final<T><<<(unsigned)ceil_div(cols, 32), 256, 0, ctx->stream>>>(
       nchunks, cols, part.as<double>(), out);
   launched(ctx);
 }

@@ -30,7 +30,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 320;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -150,13 +150,22 @@ struct Cfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES >= 4 ? 4 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
 };
 
-// C[M x N] (+bias) = op(A) op(B); or partial[z] when `part` != nullptr.
+// Persistent, warp-specialized: CTA b processes tiles b, b+grid, ... where a
+// tile is (split z, m-tile, n-tile), n fastest so the CTAs sharing an A tile
+// run concurrently (A read from HBM once).  Roles:
+//   warp 0      TMA producer over a continuous smem stage ring
+//   warp 1      TMEM alloc (2 x BN columns) + MMA issuer into accumulator
+//               buffer (tile & 1); commits free smem stages / publish tiles
+//   warps 2..5  3xTF32 split converters on every stage
+//   warps 6..9  epilogue: TMEM -> registers -> (+bias) -> global, then free
+//               the accumulator buffer -- overlaps the next tile's MMAs
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              int M, int N, int K, int kchunk, float* __restrict__ C, int ldc,
+              int M, int N, int K, int kchunk, int splits, float* __restrict__ C, int ldc,
               const float* __restrict__ bias, float* __restrict__ part) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
@@ -166,19 +175,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
   uint64_t* conv = full + S;
   uint64_t* empty = conv + S;
-  uint64_t* accum = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + S;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int k_begin = blockIdx.z * kchunk;
-  const int k_end = min(K, k_begin + kchunk);
-  const int nk = (k_end - k_begin + BK - 1) / BK;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n * splits;
 
   auto a_raw = [&](int s) { return smem + s * CF::STAGE_BYTES; };
   auto a_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + CF::A_BYTES; };
   auto b_raw = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES; };
   auto b_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES + CF::B_BYTES; };
+  // tile -> (z, m0, n0, k range)
+  auto tile_of = [&](int t, int& z, int& m0, int& n0, int& kb, int& nk) {
+    const int nt = t % num_n;
+    const int rest = t / num_n;
+    const int mt = rest % num_m;
+    z = rest / num_m;
+    m0 = mt * BM;
+    n0 = nt * BN;
+    kb = z * kchunk;
+    const int ke = min(K, kb + kchunk);
+    nk = (ke - kb + BK - 1) / BK;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -186,7 +206,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -194,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"((uint32_t)BN));
+                 "r"(CF::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -205,25 +228,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % S;
-        const uint32_t ph = (ks / S) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
-        const int kc = k_begin + ks * BK;
-        if (A_MN) {  // A stored K x M: boxes of 32 M-elements x 32 K-rows
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int z, m0, n0, kb, nk;
+        tile_of(t, z, m0, n0, kb, nk);
+        for (int ks = 0; ks < nk; ++ks, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+          const int kc = kb + ks * BK;
+          if (A_MN) {  // A stored K x M: boxes of 32 M-elements x 32 K-rows
 #pragma unroll
-          for (int b = 0; b < BM / 32; ++b)
-            tma_load_2d(a_raw(s) + b * 4096, &tmA, &full[s], m0 + 32 * b, kc);
-        } else {  // A stored M x K: one box of 32 K x 128 rows
-          tma_load_2d(a_raw(s), &tmA, &full[s], kc, m0);
-        }
-        if (B_MN) {  // B stored K x N
+            for (int b = 0; b < BM / 32; ++b)
+              tma_load_2d(a_raw(s) + b * 4096, &tmA, &full[s], m0 + 32 * b, kc);
+          } else {  // A stored M x K: one box of 32 K x 128 rows
+            tma_load_2d(a_raw(s), &tmA, &full[s], kc, m0);
+          }
+          if (B_MN) {  // B stored K x N
 #pragma unroll
-          for (int b = 0; b < BN / 32; ++b)
-            tma_load_2d(b_raw(s) + b * 4096, &tmB, &full[s], n0 + 32 * b, kc);
-        } else {  // B stored N x K
-          tma_load_2d(b_raw(s), &tmB, &full[s], kc, n0);
+            for (int b = 0; b < BN / 32; ++b)
+              tma_load_2d(b_raw(s) + b * 4096, &tmB, &full[s], n0 + 32 * b, kc);
+          } else {  // B stored N x K
+            tma_load_2d(b_raw(s), &tmB, &full[s], kc, n0);
+          }
         }
       }
     }
@@ -231,76 +259,92 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % S;
-        const uint32_t ph = (ks / S) & 1;
-        mbar_wait(&conv[s], ph);
+      int it = 0, tl = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        int z, m0, n0, kb, nk;
+        tile_of(t, z, m0, n0, kb, nk);
+        const int abuf = tl & 1;
+        mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ah = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
-        const uint32_t bh = smem_u32(b_raw(s)), bl = smem_u32(b_lo(s));
+        const uint32_t tacc = tmem + (uint32_t)(abuf * BN);
+        for (int ks = 0; ks < nk; ++ks, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ah = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
+          const uint32_t bh = smem_u32(b_raw(s)), bl = smem_u32(b_lo(s));
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          // K-major (SW128): advance 32 B inside the swizzled 128 B row; LBO
-          // unused (16 B), SBO = 1024 B between 8-row groups.
-          // MN-major (SW128_BASE32B): next 8 K-rows = 1024 B; LBO = 4096 B
-          // between 32-element MN atoms, SBO = 512 B between 4-row K groups.
-          const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
-          const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-          const uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
-          const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
-          const uint64_t dah = smem_desc(ah + aoff, alb, asb, alt);
-          const uint64_t dal = smem_desc(al + aoff, alb, asb, alt);
-          const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
-          const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
-          const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, dah, dbh, idesc, acc);
-          mma_tf32(tmem, dah, dbl, idesc, 1u);
-          mma_tf32(tmem, dal, dbh, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // K-major (SW128): advance 32 B inside the swizzled 128 B row; LBO
+            // unused (16 B), SBO = 1024 B between 8-row groups.
+            // MN-major (SW128_BASE32B): next 8 K-rows = 1024 B; LBO = 4096 B
+            // between 32-element MN atoms, SBO = 512 B between 4-row K groups.
+            const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+            const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+            const uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
+            const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
+            const uint64_t dah = smem_desc(ah + aoff, alb, asb, alt);
+            const uint64_t dal = smem_desc(al + aoff, alb, asb, alt);
+            const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
+            const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
+            const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(tacc, dah, dbh, idesc, acc);
+            mma_tf32(tacc, dah, dbl, idesc, 1u);
+            mma_tf32(tacc, dal, dbh, idesc, 1u);
+          }
+          umma_commit(&empty[s]);  // stage s free once these MMAs retire
         }
-        umma_commit(&empty[s]);  // stage s free once these MMAs retire
+        umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
       }
-      umma_commit(accum);
+    }
+  } else if (warp < 6) {
+    // ---------------- split converters ----------------
+    const int ctid = threadIdx.x - 64;  // 0..127
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int z, m0, n0, kb, nk;
+      tile_of(t, z, m0, n0, kb, nk);
+      for (int ks = 0; ks < nk; ++ks, ++it) {
+        const int s = it % S;
+        const uint32_t ph = (it / S) & 1;
+        mbar_wait(&full[s], ph);
+        split_tile(reinterpret_cast<float4*>(a_raw(s)), reinterpret_cast<float4*>(a_lo(s)),
+                   CF::A_BYTES / 16, ctid, 128);
+        split_tile(reinterpret_cast<float4*>(b_raw(s)), reinterpret_cast<float4*>(b_lo(s)),
+                   CF::B_BYTES / 16, ctid, 128);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
     }
   } else {
-    // ---------------- split converters, then epilogue ----------------
-    const int ctid = threadIdx.x - 64;  // 0..127
-    for (int ks = 0; ks < nk; ++ks) {
-      const int s = ks % S;
-      const uint32_t ph = (ks / S) & 1;
-      mbar_wait(&full[s], ph);
-      split_tile(reinterpret_cast<float4*>(a_raw(s)), reinterpret_cast<float4*>(a_lo(s)),
-                 CF::A_BYTES / 16, ctid, 128);
-      split_tile(reinterpret_cast<float4*>(b_raw(s)), reinterpret_cast<float4*>(b_lo(s)),
-                 CF::B_BYTES / 16, ctid, 128);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
-    }
-    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (one output row per thread)
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---------------- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 ----------------
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
     const bool vec = ((ldc & 3) == 0) && ((N & 3) == 0);
+    int tl = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      int z, m0, n0, kb, nk;
+      tile_of(t, z, m0, n0, kb, nk);
+      const int abuf = tl & 1;
+      mbar_wait(&tfull[abuf], (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = m0 + q * 32 + lane;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
-      if (row >= M) continue;
-      const int col0 = n0 + c;
-      if (part) {
-        float* dst = part + ((int64_t)blockIdx.z * M + row) * N;
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < N) dst[col0 + j] = __uint_as_float(r[j]);
-      } else {
-        float* dst = C + (int64_t)row * ldc;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
+        if (row >= M) continue;
+        const int col0 = n0 + c;
+        float* dst = part ? part + ((int64_t)z * M + row) * N : C + (int64_t)row * ldc;
+        const float* bb = part ? nullptr : bias;
         if (vec && col0 + 32 <= N) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-            if (bias) {
-              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0 + j));
+            if (bb) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(bb + col0 + j));
               v.x = __fadd_rn(v.x, b.x);
               v.y = __fadd_rn(v.y, b.y);
               v.z = __fadd_rn(v.z, b.z);
@@ -311,10 +355,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
           for (int j = 0; j < 32; ++j)
             if (col0 + j < N)
-              dst[col0 + j] = bias ? __fadd_rn(__uint_as_float(r[j]), bias[col0 + j])
-                                   : __uint_as_float(r[j]);
+              dst[col0 + j] = bb ? __fadd_rn(__uint_as_float(r[j]), bb[col0 + j])
+                                 : __uint_as_float(r[j]);
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[abuf]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -322,7 +369,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"((uint32_t)BN));
+                 "r"(CF::TMEM_COLS));
   }
 }
 
@@ -381,8 +428,10 @@ static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb, i
     SGNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
-  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, C, N, bias, part);
+  const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * splits;
+  const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, splits, C, N, bias,
+                                                  part);
   launched(ctx);
 }
 

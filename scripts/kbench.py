@@ -1,0 +1,38 @@
+"""Dev microbenchmark: time individual library kernels on Arxiv shapes (CUDA events,
+L2 flushed between iterations)."""
+import os, sys, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2308_12093_b200 import device as d
+
+n, m, k = 169343, 128, 256
+dev = torch.device("cuda")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+X = torch.randn(n, m, device=dev)
+G = torch.randn(n, k, device=dev)
+th = torch.randn(m, k, device=dev)
+out = torch.empty(n, k, device=dev)
+outm = torch.empty(n, m, device=dev)
+
+def t(fn, iters=20):
+    for _ in range(3): fn()
+    ms = []
+    for _ in range(iters):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
+    return statistics.median(ms) * 1e3
+
+which = sys.argv[1:] or ["nn", "tn", "nt", "colsum"]
+for w in which:
+    if w == "nn":
+        us = t(lambda: d.gemm(X, th)); byt = 4 * (n * m + n * k)
+    elif w == "tn":
+        us = t(lambda: d.gemm(X, G, True, False)); byt = 4 * (n * m + n * k)
+    elif w == "nt":
+        us = t(lambda: d.gemm(G, th, False, True)); byt = 4 * (n * m + n * k)
+    elif w == "colsum":
+        us = t(lambda: d.column_sums(G)); byt = 4 * n * k
+    elif w == "copy":
+        us = t(lambda: out.copy_(G)); byt = 8 * n * k
+    print(f"{w}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s", flush=True)
