@@ -125,15 +125,40 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Split a raw fp32 tile in place into hi (tf32-exact) and write lo.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+
+// Split a raw fp32 smem tile in place into hi (tf32-exact) and write lo.
 __device__ __forceinline__ void split_tile(float4* raw, float4* lo, int n4, int tid, int nthr) {
   for (int i = tid; i < n4; i += nthr) {
     float4 v = raw[i];
     float4 h, l;
-    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    h.x = __uint_as_float(tf32_hi(v.x));
+    h.y = __uint_as_float(tf32_hi(v.y));
+    h.z = __uint_as_float(tf32_hi(v.z));
+    h.w = __uint_as_float(tf32_hi(v.w));
     l.x = __fsub_rn(v.x, h.x);
     l.y = __fsub_rn(v.y, h.y);
     l.z = __fsub_rn(v.z, h.z);
@@ -143,40 +168,59 @@ __device__ __forceinline__ void split_tile(float4* raw, float4* lo, int n4, int 
   }
 }
 
+__global__ void k_split_global(int64_t n, const float* __restrict__ x, float* __restrict__ hi,
+                               float* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const float h = __uint_as_float(tf32_hi(v));
+    hi[i] = h;
+    lo[i] = __fsub_rn(v, h);
+  }
+}
+
 template <int BN>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+  static constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A tile
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A raw | B hi | B lo
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES >= 4 ? 4 : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  static constexpr int NA = 2;                                // TMEM A buffers (hi|lo, 64 cols)
+  static constexpr uint32_t USED = 2 * BN + NA * 64;          // accumulators + A buffers
+  static constexpr uint32_t TMEM_COLS = USED <= 256 ? 256 : 512;
 };
 
 // Persistent, warp-specialized: CTA b processes tiles b, b+grid, ... where a
 // tile is (split z, m-tile, n-tile), n fastest so the CTAs sharing an A tile
 // run concurrently (A read from HBM once).  Roles:
-//   warp 0      TMA producer over a continuous smem stage ring
-//   warp 1      TMEM alloc (2 x BN columns) + MMA issuer into accumulator
-//               buffer (tile & 1); commits free smem stages / publish tiles
-//   warps 2..5  3xTF32 split converters on every stage
-//   warps 6..9  epilogue: TMEM -> registers -> (+bias) -> global, then free
-//               the accumulator buffer -- overlaps the next tile's MMAs
-template <bool A_MN, bool B_MN, int BN>
+//   warp 0      TMA producer over a continuous smem stage ring (A raw, B hi/lo
+//               -- B pre-split in global when small, else raw + split here)
+//   warp 1      TMEM alloc + MMA issuer: A (hi, lo) from TMEM, B from smem,
+//               D in one of two TMEM accumulators (tile & 1)
+//   warps 2..5  converters: thread = one A row = one TMEM lane; reads its row
+//               from smem, splits hi/lo in registers and tcgen05.st's both into
+//               a TMEM A buffer (no smem write-back); splits B in smem if needed
+//   warps 6..9  epilogue: TMEM -> registers -> (+bias) -> global, overlapping
+//               the next tile's MMAs
+template <bool A_MN, bool B_MN, int BN, bool B_PRE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              int M, int N, int K, int kchunk, int splits, float* __restrict__ C, int ldc,
-              const float* __restrict__ bias, float* __restrict__ part) {
+              const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kchunk,
+              int splits, float* __restrict__ C, int ldc, const float* __restrict__ bias,
+              float* __restrict__ part) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
+  constexpr int NA = CF::NA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
-  uint64_t* conv = full + S;
-  uint64_t* empty = conv + S;
-  uint64_t* tfull = empty + S;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
+  uint64_t* empty = full + S;
+  uint64_t* afull = empty + S;    // [NA] converters -> MMA
+  uint64_t* aempty = afull + NA;  // [NA] MMA -> converters
+  uint64_t* tfull = aempty + NA;  // [2]
+  uint64_t* tempty = tfull + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -184,10 +228,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int tiles = num_m * num_n * splits;
 
   auto a_raw = [&](int s) { return smem + s * CF::STAGE_BYTES; };
-  auto a_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + CF::A_BYTES; };
-  auto b_raw = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES; };
-  auto b_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES + CF::B_BYTES; };
-  // tile -> (z, m0, n0, k range)
+  auto b_hi = [&](int s) { return smem + s * CF::STAGE_BYTES + CF::A_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * CF::STAGE_BYTES + CF::A_BYTES + CF::B_BYTES; };
   auto tile_of = [&](int t, int& z, int& m0, int& n0, int& kb, int& nk) {
     const int nt = t % num_n;
     const int rest = t / num_n;
@@ -203,8 +245,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NA; ++a) {
+      mbar_init(&afull[a], 4);
+      mbar_init(&aempty[a], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -224,6 +269,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + 2 * BN;  // A buffers after the two accumulators
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -236,7 +282,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+          mbar_expect_tx(&full[s], CF::A_BYTES + (B_PRE ? 2 : 1) * CF::B_BYTES);
           const int kc = kb + ks * BK;
           if (A_MN) {  // A stored K x M: boxes of 32 M-elements x 32 K-rows
 #pragma unroll
@@ -247,10 +293,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (B_MN) {  // B stored K x N
 #pragma unroll
-            for (int b = 0; b < BN / 32; ++b)
-              tma_load_2d(b_raw(s) + b * 4096, &tmB, &full[s], n0 + 32 * b, kc);
+            for (int b = 0; b < BN / 32; ++b) {
+              tma_load_2d(b_hi(s) + b * 4096, &tmB, &full[s], n0 + 32 * b, kc);
+              if (B_PRE) tma_load_2d(b_lo(s) + b * 4096, &tmBlo, &full[s], n0 + 32 * b, kc);
+            }
           } else {  // B stored N x K
-            tma_load_2d(b_raw(s), &tmB, &full[s], kc, n0);
+            tma_load_2d(b_hi(s), &tmB, &full[s], kc, n0);
+            if (B_PRE) tma_load_2d(b_lo(s), &tmBlo, &full[s], kc, n0);
           }
         }
       }
@@ -258,7 +307,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+      constexpr uint32_t idesc = instr_desc(BN, false, B_MN);  // A from TMEM is K-major
       int it = 0, tl = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
         int z, m0, n0, kb, nk;
@@ -268,54 +317,83 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tacc = tmem + (uint32_t)(abuf * BN);
         for (int ks = 0; ks < nk; ++ks, ++it) {
-          const int s = it % S;
-          const uint32_t ph = (it / S) & 1;
-          mbar_wait(&conv[s], ph);
+          const int s = it % S, a = it % NA;
+          mbar_wait(&afull[a], (it / NA) & 1);  // implies full[s] (converters waited on it)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ah = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
-          const uint32_t bh = smem_u32(b_raw(s)), bl = smem_u32(b_lo(s));
+          const uint32_t ta = tmem_a + (uint32_t)(a * 64);
+          const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            // K-major (SW128): advance 32 B inside the swizzled 128 B row; LBO
-            // unused (16 B), SBO = 1024 B between 8-row groups.
-            // MN-major (SW128_BASE32B): next 8 K-rows = 1024 B; LBO = 4096 B
-            // between 32-element MN atoms, SBO = 512 B between 4-row K groups.
-            const uint32_t aoff = A_MN ? kk * 1024 : kk * 32;
+            // B K-major (SW128): +32 B inside the swizzled row, SBO 1024.
+            // B MN-major (SW128_BASE32B): +1024 B per 8 K-rows, LBO 4096, SBO 512.
             const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-            const uint32_t alb = A_MN ? 4096 : 16, asb = A_MN ? 512 : 1024, alt = A_MN ? 1 : 2;
             const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
-            const uint64_t dah = smem_desc(ah + aoff, alb, asb, alt);
-            const uint64_t dal = smem_desc(al + aoff, alb, asb, alt);
             const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
             const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
             const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(tacc, dah, dbh, idesc, acc);
-            mma_tf32(tacc, dah, dbl, idesc, 1u);
-            mma_tf32(tacc, dal, dbh, idesc, 1u);
+            mma_tf32_ts(tacc, ta + kk * 8, dbh, idesc, acc);       // hi . hi
+            mma_tf32_ts(tacc, ta + kk * 8, dbl, idesc, 1u);        // hi . lo
+            mma_tf32_ts(tacc, ta + 32 + kk * 8, dbh, idesc, 1u);   // lo . hi
           }
-          umma_commit(&empty[s]);  // stage s free once these MMAs retire
+          umma_commit(&empty[s]);   // smem stage free
+          umma_commit(&aempty[a]);  // TMEM A buffer free
         }
         umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
       }
     }
   } else if (warp < 6) {
-    // ---------------- split converters ----------------
-    const int ctid = threadIdx.x - 64;  // 0..127
+    // ---------------- converters: one A row per thread -> TMEM lane ----------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // tile row == TMEM lane
+    const int ctid = threadIdx.x - 64;
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int z, m0, n0, kb, nk;
       tile_of(t, z, m0, n0, kb, nk);
       for (int ks = 0; ks < nk; ++ks, ++it) {
-        const int s = it % S;
-        const uint32_t ph = (it / S) & 1;
-        mbar_wait(&full[s], ph);
-        split_tile(reinterpret_cast<float4*>(a_raw(s)), reinterpret_cast<float4*>(a_lo(s)),
-                   CF::A_BYTES / 16, ctid, 128);
-        split_tile(reinterpret_cast<float4*>(b_raw(s)), reinterpret_cast<float4*>(b_lo(s)),
-                   CF::B_BYTES / 16, ctid, 128);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int s = it % S, a = it % NA;
+        mbar_wait(&full[s], (it / S) & 1);
+        if (!B_PRE) {
+          split_tile(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
+                     CF::B_BYTES / 16, ctid, 128);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        float v[32];
+        const uint8_t* base = a_raw(s);
+        if (A_MN) {
+          // 4 boxes of 32 M x 32 K-rows; 32 B chunks swizzled with (K-row % 4)
+          const uint8_t* bx = base + (r >> 5) * 4096;
+          const int p = r & 31, c32 = p >> 3, e = p & 7;
+#pragma unroll
+          for (int kr = 0; kr < 32; ++kr)
+            v[kr] = *reinterpret_cast<const float*>(bx + kr * 128 + ((c32 ^ (kr & 3)) << 5) + e * 4);
+        } else {
+          // row r: 128 B, 16 B chunks swizzled with (row % 8)
+          const uint8_t* row = base + r * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 x = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+            v[4 * c] = x.x;
+            v[4 * c + 1] = x.y;
+            v[4 * c + 2] = x.z;
+            v[4 * c + 3] = x.w;
+          }
+        }
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          hi[j] = tf32_hi(v[j]);
+          lo[j] = __float_as_uint(__fsub_rn(v[j], __uint_as_float(hi[j])));
+        }
+        mbar_wait(&aempty[a], ((it / NA) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem_a + (uint32_t)(a * 64) + ((uint32_t)(q * 32) << 16);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
+        if (lane == 0) mbar_arrive(&afull[a]);
       }
     }
   } else {
@@ -418,10 +496,11 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t o
   return r == CUDA_SUCCESS;
 }
 
-template <bool A_MN, bool B_MN, int BN>
-static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
-                   int K, int splits, int kchunk, float* C, const float* bias, float* part) {
-  auto kern = k_gemm_tc<A_MN, B_MN, BN>;
+template <bool A_MN, bool B_MN, int BN, bool B_PRE>
+static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb,
+                   const CUtensorMap& mbl, int M, int N, int K, int splits, int kchunk, float* C,
+                   const float* bias, float* part) {
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE>;
   const int smem = Cfg<BN>::SMEM;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -430,19 +509,29 @@ static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb, i
   }
   const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * splits;
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
-  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, M, N, K, kchunk, splits, C, N, bias,
-                                                  part);
+  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, mbl, M, N, K, kchunk, splits, C, N,
+                                                  bias, part);
   launched(ctx);
 }
 
 template <int BN>
-static void dispatch_major(sgnn_ctx ctx, bool a_mn, bool b_mn, const CUtensorMap& ma,
-                           const CUtensorMap& mb, int M, int N, int K, int splits, int kchunk,
-                           float* C, const float* bias, float* part) {
-  if (a_mn && b_mn) launch<true, true, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
-  else if (a_mn) launch<true, false, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
-  else if (b_mn) launch<false, true, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
-  else launch<false, false, BN>(ctx, ma, mb, M, N, K, splits, kchunk, C, bias, part);
+static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const CUtensorMap& ma,
+                     const CUtensorMap& mb, const CUtensorMap& mbl, int M, int N, int K,
+                     int splits, int kchunk, float* C, const float* bias, float* part) {
+#define L(AM, BM_, PR) \
+  launch<AM, BM_, BN, PR>(ctx, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, part)
+  if (pre) {
+    if (a_mn && b_mn) L(true, true, true);
+    else if (a_mn) L(true, false, true);
+    else if (b_mn) L(false, true, true);
+    else L(false, false, true);
+  } else {
+    if (a_mn && b_mn) L(true, true, false);
+    else if (a_mn) L(true, false, false);
+    else if (b_mn) L(false, true, false);
+    else L(false, false, false);
+  }
+#undef L
 }
 
 }  // namespace tc
@@ -470,12 +559,30 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   if ((reinterpret_cast<uintptr_t>(C) & 15) || (bias && (reinterpret_cast<uintptr_t>(bias) & 15)))
     return false;
   const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
-  CUtensorMap ma, mb;
   const bool a_mn = ta, b_mn = !tb;
+  // Small B (the parameter matrix Theta): split hi/lo once in global memory so
+  // the kernel streams both halves with TMA and spends no smem bandwidth on it.
+  const int64_t belems = (int64_t)rb * cb;
+  const bool pre = belems * 8 <= (int64_t)ra * ca;
+  DevBuf bsplit;
+  const float* Bhi = B;
+  const float* Blo = B;
+  if (pre) {
+    bsplit = DevBuf((size_t)belems * 8, ctx->stream);
+    k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
+        belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);
+    launched(ctx);
+    Bhi = bsplit.as<float>();
+    Blo = bsplit.as<float>() + belems;
+  }
+  CUtensorMap ma, mb, mbl;
   // A: ta -> stored K x M (MN-major), else M x K (K-major)
-  const bool okA = a_mn ? make_map(&ma, A, M, K, ca, BK, true) : make_map(&ma, A, K, M, ca, BM, false);
+  const bool okA =
+      a_mn ? make_map(&ma, A, M, K, ca, BK, true) : make_map(&ma, A, K, M, ca, BM, false);
   // B: tb -> stored N x K (K-major), else K x N (MN-major)
-  const bool okB = b_mn ? make_map(&mb, B, N, K, cb, BK, true) : make_map(&mb, B, K, N, cb, BN, false);
+  bool okB = b_mn ? make_map(&mb, Bhi, N, K, cb, BK, true) : make_map(&mb, Bhi, K, N, cb, BN, false);
+  okB = okB && (b_mn ? make_map(&mbl, Blo, N, K, cb, BK, true)
+                     : make_map(&mbl, Blo, K, N, cb, BN, false));
   if (!okA || !okB) return false;
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
   int splits = 1;
@@ -493,9 +600,9 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     pp = part.as<float>();
   }
   switch (BN) {
-    case 32: dispatch_major<32>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
-    case 64: dispatch_major<64>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
-    default: dispatch_major<128>(ctx, a_mn, b_mn, ma, mb, M, N, K, splits, kchunk, C, bias, pp); break;
+    case 32: dispatch<32>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
+    case 64: dispatch<64>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
+    default: dispatch<128>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
   }
   if (splits > 1) {
     const int64_t MN = (int64_t)M * N;
