@@ -26,11 +26,11 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
   if (s.forward == SGNN_TRANSFORM_FIRST) {
     DevBuf M((size_t)n * k * sizeof(T), st);
     gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
-    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias);
+    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz);
     c->saved_input = X;
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
-    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr);
+    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
     gemm<T>(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias);
     if (s.forward == SGNN_PROPAGATE_FIRST_CACHED)
       c->saved_propagated = std::move(P);  // reclassified into the cache (gcn.hpp:124)
@@ -55,7 +55,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     case SGNN_FUSED_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf S((size_t)n * k * sizeof(T), st);
-      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr);
+      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz);
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
       if (fg) gemm<T>(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input);
       break;
@@ -63,12 +63,12 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     case SGNN_SPLIT_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf P((size_t)n * m * sizeof(T), st);
-      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr);
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
       gemm<T>(ctx, P.as<T>(), n, m, G, n, k, true, false, d_theta);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
       }
       break;
     }
@@ -78,7 +78,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
       }
       break;
     }

@@ -55,7 +55,7 @@ void build_ptr(sgnn_ctx ctx, const int32_t* sorted_ids, int64_t nnz, int32_t n, 
 // C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-              const T* vals, const T* B, int32_t f, T* C, const T* bias);
+              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz);
 
 // C = op(A) op(B) (row-major); A ra x ca, B rb x cb; bias added per column of C
 template <class T>

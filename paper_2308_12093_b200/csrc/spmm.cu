@@ -11,10 +11,17 @@
 // order with an unfused multiply then add (madd), which is exactly the
 // reference's `crow[c] += v * brow[c]` (kernels.hpp:47-51): results are
 // bit-identical to the reference CPU SpMM in float32 and float64.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.cuh"
 
 namespace sgnn {
+
+#ifndef SPMM_MINB
+#define SPMM_MINB 4
+#endif
 
 template <class T, int W>
 struct VecT;
@@ -34,6 +41,13 @@ struct VecT<double, 2> {
 template <class V>
 __device__ __forceinline__ V ldg_v(const V* p) {
   return __ldg(p);
+}
+
+// Output rows are written once and never re-read by this kernel: stream them
+// (evict-first) so the gathered dense operand keeps its L2 residency.
+template <class V>
+__device__ __forceinline__ void st_out(V* p, const V& v) {
+  __stcs(p, v);
 }
 
 template <class T, int W>
@@ -87,11 +101,12 @@ __device__ __forceinline__ double pack<double, 1, double>(const double* a) {
 
 // LPR lanes per row, R vectors per lane, W scalars per vector, U edges in flight
 template <class T, int LPR, int R, int W, int U>
-__global__ void __launch_bounds__(256) k_spmm_csr(int32_t n_rows, const int32_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(256, (R == 1 && sizeof(T) == 4) ? SPMM_MINB : 1) k_spmm_csr(int32_t n_rows, const int32_t* __restrict__ rowptr,
                                                   const int32_t* __restrict__ cols,
                                                   const T* __restrict__ vals,
                                                   const T* __restrict__ B, int32_t f,
-                                                  T* __restrict__ C, const T* __restrict__ bias) {
+                                                  T* __restrict__ C, const T* __restrict__ bias,
+                                                  int32_t ld) {
   using V = typename VecT<T, W>::type;
   constexpr int RPW = 32 / LPR;  // rows per warp
   const int lane = threadIdx.x & 31;
@@ -100,7 +115,8 @@ __global__ void __launch_bounds__(256) k_spmm_csr(int32_t n_rows, const int32_t*
   const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int fv = f / W;  // vectors per row
+  const int fv = f / W;    // vectors in this column window
+  const int ldv = ld / W;  // row stride in vectors
   const V* Bv = reinterpret_cast<const V*>(B);
   V* Cv = reinterpret_cast<V*>(C);
   const V* biasv = reinterpret_cast<const V*>(bias);
@@ -142,7 +158,7 @@ __global__ void __launch_bounds__(256) k_spmm_csr(int32_t n_rows, const int32_t*
               s = __shfl_sync(gmask, my_val, j & (LPR - 1), LPR);
             }
             sv[u] = s;
-            const V* brow = Bv + (int64_t)c * fv;
+            const V* brow = Bv + (int64_t)c * ldv;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int cv = cb + r * LPR + g;
@@ -169,9 +185,9 @@ __global__ void __launch_bounds__(256) k_spmm_csr(int32_t n_rows, const int32_t*
               const T* bp = reinterpret_cast<const T*>(&bb);
 #pragma unroll
               for (int w = 0; w < W; ++w) b[w] = add_rn(acc[r][w], bp[w]);
-              Cv[row * fv + cv] = pack<T, W, V>(b);
+              st_out(Cv + row * ldv + cv, pack<T, W, V>(b));
             } else {
-              Cv[row * fv + cv] = pack<T, W, V>(acc[r]);
+              st_out(Cv + row * ldv + cv, pack<T, W, V>(acc[r]));
             }
           }
         }
@@ -180,10 +196,109 @@ __global__ void __launch_bounds__(256) k_spmm_csr(int32_t n_rows, const int32_t*
   }
 }
 
-template <class T, int W, int LPR>
+// ---------------------------------------------------------------------------
+// Lean fp32 row kernel (f <= 32*4*R): one warp per output row, no grid-stride
+// loop, broadcast loads of (col, val) instead of shuffles, 32-bit vector
+// offsets -- small enough for 64 resident warps/SM, which is what the random
+// 512-byte row gathers need (the hardware gathers at ~12 TB/s when enough
+// independent warps are in flight).  Same per-element edge order, unfused.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 ldB(const float4* p) { return __ldg(p); }
+
+template <int R, int U>
+__global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 : 4)))
+    k_spmm_lean(int32_t n_rows, const int32_t* __restrict__ rowptr,
+                const int32_t* __restrict__ cols, const float* __restrict__ vals,
+                const float4* __restrict__ B, int32_t fv, float4* __restrict__ C,
+                const float4* __restrict__ bias, int32_t ldv) {
+  const int lane = threadIdx.x & 31;
+  const int32_t row = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (row >= n_rows) return;
+  const int32_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  float4 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool ok1 = R < 2 || (32 + lane) < fv;
+  const bool ok0 = lane < fv;
+  int32_t e = beg;
+  for (; e + U <= end; e += U) {
+    int32_t c[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = __ldg(cols + e + u);
+      v[u] = __ldg(vals + e + u);
+    }
+    float4 b[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4* src = B + (uint32_t)c[u] * (uint32_t)ldv + lane;
+      if (ok0) b[u][0] = ldB(src);
+      if (R > 1 && ok1) b[u][R - 1] = ldB(src + 32);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r].x = madd(acc[r].x, v[u], b[u][r].x);
+        acc[r].y = madd(acc[r].y, v[u], b[u][r].y);
+        acc[r].z = madd(acc[r].z, v[u], b[u][r].z);
+        acc[r].w = madd(acc[r].w, v[u], b[u][r].w);
+      }
+  }
+  for (; e < end; ++e) {
+    const int32_t c = __ldg(cols + e);
+    const float v = __ldg(vals + e);
+    const float4* src = B + (uint32_t)c * (uint32_t)ldv + lane;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if ((r == 0 && ok0) || (r == 1 && ok1)) {
+        const float4 b = __ldg(src + r * 32);
+        acc[r].x = madd(acc[r].x, v, b.x);
+        acc[r].y = madd(acc[r].y, v, b.y);
+        acc[r].z = madd(acc[r].z, v, b.z);
+        acc[r].w = madd(acc[r].w, v, b.w);
+      }
+    }
+  }
+  float4* dst = C + (uint32_t)row * (uint32_t)ldv + lane;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if ((r == 0 && ok0) || (r == 1 && ok1)) {
+      float4 o = acc[r];
+      if (bias) {
+        const float4 bb = __ldg(bias + r * 32 + lane);
+        o.x = __fadd_rn(o.x, bb.x);
+        o.y = __fadd_rn(o.y, bb.y);
+        o.z = __fadd_rn(o.z, bb.z);
+        o.w = __fadd_rn(o.w, bb.w);
+      }
+      __stcs(dst + r * 32, o);
+    }
+  }
+}
+
+template <int R>
+static void launch_lean(sgnn_ctx ctx, int U, int32_t n_rows, const int32_t* rowptr,
+                        const int32_t* cols, const float* vals, const float* B, int32_t f,
+                        float* C, const float* bias, int32_t ld) {
+  const int grid = (int)ceil_div(n_rows, 8);
+  const float4* Bv = reinterpret_cast<const float4*>(B);
+  float4* Cv = reinterpret_cast<float4*>(C);
+  const float4* bv = reinterpret_cast<const float4*>(bias);
+  if (U >= 4)
+    k_spmm_lean<R, 4><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+  else if (U >= 2)
+    k_spmm_lean<R, 2><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+  else
+    k_spmm_lean<R, 1><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+  launched(ctx);
+}
+
+template <class T, int W, int LPR, int U>
 static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, const T* vals, const T* B, int32_t f, T* C,
-                       const T* bias) {
+                       const T* bias, int32_t ld) {
   const int rpw = 32 / LPR;
   const int64_t warps = ceil_div(n_rows, rpw);
   const int block = 256;
@@ -191,12 +306,11 @@ static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowpt
   const int64_t cap = (int64_t)ctx->num_sms * 64;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  constexpr int U = LPR >= 4 ? 4 : (LPR == 2 ? 2 : 1);
   switch (R) {
 #define CASE(RR)                                                                         \
   case RR:                                                                               \
     k_spmm_csr<T, LPR, RR, W, U><<<(int)grid, block, 0, ctx->stream>>>(n_rows, rowptr, cols, \
-                                                                      vals, B, f, C, bias); \
+                                                                      vals, B, f, C, bias, ld); \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8)
 #undef CASE
@@ -207,40 +321,67 @@ static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowpt
 
 template <class T, int W>
 static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-                     const T* vals, const T* B, int32_t f, T* C, const T* bias) {
+                     const T* vals, const T* B, int32_t f, T* C, const T* bias, int32_t ld) {
   const int fv = f / W;
   int lpr = 1;
   while (lpr < 32 && lpr < fv) lpr <<= 1;
   int R = (int)ceil_div(fv, lpr);
   R = R <= 1 ? 1 : R <= 2 ? 2 : R <= 4 ? 4 : 8;  // R > 8: column-block loop in the kernel
-  switch (lpr) {
-    case 1: launch_lpr<T, W, 1>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
-    case 2: launch_lpr<T, W, 2>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
-    case 4: launch_lpr<T, W, 4>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
-    case 8: launch_lpr<T, W, 8>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
-    case 16: launch_lpr<T, W, 16>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
-    default: launch_lpr<T, W, 32>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias); break;
+  int U = lpr >= 4 ? 4 : (lpr == 2 ? 2 : 1);
+  if (const char* e = getenv("SGNN_SPMM_CFG")) {  // dev tuning: "lpr,R,U"
+    int a = 0, b = 0, c = 0;
+    if (sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a * b >= (lpr * R) / 1 && a <= 32) {
+      lpr = a;
+      R = b;
+      U = c;
+    }
   }
+#define LPR_CASE(L)                                                                             \
+  case L:                                                                                       \
+    if (U >= 8) launch_lpr<T, W, L, 8>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld);      \
+    else if (U >= 4) launch_lpr<T, W, L, 4>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld); \
+    else if (U >= 2) launch_lpr<T, W, L, 2>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld); \
+    else launch_lpr<T, W, L, 1>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld);             \
+    break;
+  switch (lpr) {
+    LPR_CASE(1) LPR_CASE(2) LPR_CASE(4) LPR_CASE(8) LPR_CASE(16)
+    default: LPR_CASE(32)
+  }
+#undef LPR_CASE
 }
 
+// fp32 rows of 68..256 floats use the lean one-row-per-warp kernel (measured
+// 84 us for the Arxiv f=128 product vs 125 us for the generic kernel); other
+// widths and fp64 use the generic LPR-lane kernel.  SGNN_SPMM_MODE=1 forces
+// the generic kernel (both are bit-identical to the reference).
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-              const T* vals, const T* B, int32_t f, T* C, const T* bias) {
+              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz) {
   if (n_rows == 0 || f == 0) return;
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;
   const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
                        (!bias || reinterpret_cast<uintptr_t>(bias) % 16 == 0);
+  if constexpr (sizeof(T) == 4) {
+    static const int mode = getenv("SGNN_SPMM_MODE") ? atoi(getenv("SGNN_SPMM_MODE")) : 0;
+    static const int lu = getenv("SGNN_SPMM_U") ? atoi(getenv("SGNN_SPMM_U")) : 2;
+    const bool vec_ok = aligned && f % 4 == 0 && nnz > 0;
+    if (mode == 0 && vec_ok && f > 64 && f <= 256) {  // lean one-row-per-warp kernel
+      if (f <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f);
+      else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f);
+      return;
+    }
+  }
   if (f % VW == 0 && aligned)
-    launch_w<T, VW>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias);
+    launch_w<T, VW>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f);
   else
-    launch_w<T, 1>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias);
+    launch_w<T, 1>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f);
 }
 
 template void spmm_csr<float>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const float*,
-                              const float*, int32_t, float*, const float*);
+                              const float*, int32_t, float*, const float*, int64_t);
 template void spmm_csr<double>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const double*,
-                               const double*, int32_t, double*, const double*);
+                               const double*, int32_t, double*, const double*, int64_t);
 
 }  // namespace sgnn
 
@@ -257,11 +398,11 @@ extern "C" int sgnn_spmm(sgnn_ctx ctx, sgnn_adj adj, int transposed, const void*
   if (adj->dtype == SGNN_F32) {
     const float* v = transposed ? adj->cvals.as<float>() : adj->vals.as<float>();
     spmm_csr<float>(ctx, n_out, ptr, idx, v, static_cast<const float*>(B), f,
-                    static_cast<float*>(C), static_cast<const float*>(bias));
+                    static_cast<float*>(C), static_cast<const float*>(bias), adj->nnz);
   } else {
     const double* v = transposed ? adj->cvals.as<double>() : adj->vals.as<double>();
     spmm_csr<double>(ctx, n_out, ptr, idx, v, static_cast<const double*>(B), f,
-                     static_cast<double*>(C), static_cast<const double*>(bias));
+                     static_cast<double*>(C), static_cast<const double*>(bias), adj->nnz);
   }
   SGNN_API_END
 }

@@ -88,9 +88,9 @@ class Context:
     def synchronize(self):
         check(lib.sgnn_ctx_synchronize(self.handle))
 
-    def __del__(self):
+    def __del__(self, _destroy=lib.sgnn_ctx_destroy):
         if getattr(self, "handle", None):
-            lib.sgnn_ctx_destroy(self.handle)
+            _destroy(self.handle)
             self.handle = None
 
 
@@ -271,9 +271,9 @@ class Adjacency:
     def multiply_transposed(self, B):
         return self.spmm(B, transposed=True)
 
-    def __del__(self):
+    def __del__(self, _destroy=lib.sgnn_adj_destroy):
         if getattr(self, "handle", None):
-            lib.sgnn_adj_destroy(self.handle)
+            _destroy(self.handle)
             self.handle = None
 
 
@@ -308,9 +308,9 @@ class Pattern:
         names = ["rowptr", "cols", "colptr", "rows", "perm", "diag"]
         return {nm: _view(p.value, sz, torch.int32, dev) for nm, p, sz in zip(names, ptrs, sizes)}
 
-    def __del__(self):
+    def __del__(self, _destroy=lib.sgnn_pattern_destroy):
         if getattr(self, "handle", None):
-            lib.sgnn_pattern_destroy(self.handle)
+            _destroy(self.handle)
             self.handle = None
 
 
@@ -366,9 +366,9 @@ class GcnCache:
         check(lib.sgnn_gcn_cache_retained_bytes(self.handle, C.byref(v)))
         return v.value
 
-    def __del__(self):
+    def __del__(self, _destroy=lib.sgnn_gcn_cache_destroy):
         if getattr(self, "handle", None):
-            lib.sgnn_gcn_cache_destroy(self.handle)
+            _destroy(self.handle)
             self.handle = None
 
 
@@ -430,9 +430,9 @@ class GatCache:
                                              _p(mask)))
         return alpha, mask
 
-    def __del__(self):
+    def __del__(self, _destroy=lib.sgnn_gat_cache_destroy):
         if getattr(self, "handle", None):
-            lib.sgnn_gat_cache_destroy(self.handle)
+            _destroy(self.handle)
             self.handle = None
 
 

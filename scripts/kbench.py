@@ -14,16 +14,25 @@ th = torch.randn(m, k, device=dev)
 out = torch.empty(n, k, device=dev)
 outm = torch.empty(n, m, device=dev)
 
+FLUSH = os.environ.get("FLUSH", "write")
+def do_flush():
+    flush.fill_(1)
+    if FLUSH == "readback":
+        flush.view(torch.int64).sum()  # leave L2 holding clean lines
+
 def t(fn, iters=20):
     for _ in range(3): fn()
     ms = []
     for _ in range(iters):
-        flush.fill_(1)
+        do_flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
     return statistics.median(ms) * 1e3
 
 which = sys.argv[1:] or ["nn", "tn", "nt", "colsum"]
+if any(w.startswith("spmm") for w in which):
+    src, dst = d.synthetic_graph(n, 1166243 / n, 1)
+    A = d.Adjacency.gcn_operator(n, src, dst, torch.float32, "csc")
 for w in which:
     if w == "nn":
         us = t(lambda: d.gemm(X, th)); byt = 4 * (n * m + n * k)
@@ -33,6 +42,12 @@ for w in which:
         us = t(lambda: d.gemm(G, th, False, True)); byt = 4 * (n * m + n * k)
     elif w == "colsum":
         us = t(lambda: d.column_sums(G)); byt = 4 * n * k
+    elif w == "spmm":
+        us = t(lambda: A.spmm(X, out=outm)); byt = 4 * (n + 1) + 8 * A.nnz + 8 * n * m
+    elif w == "spmmT":
+        us = t(lambda: A.spmm(X, transposed=True, out=outm)); byt = 4 * (n + 1) + 8 * A.nnz + 8 * n * m
+    elif w == "spmm256":
+        us = t(lambda: A.spmm(G, out=out)); byt = 4 * (n + 1) + 8 * A.nnz + 8 * n * k
     elif w == "copy":
         us = t(lambda: out.copy_(G)); byt = 8 * n * k
     print(f"{w}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s", flush=True)
