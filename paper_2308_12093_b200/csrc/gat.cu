@@ -16,6 +16,7 @@
 // unfused multiply-add), so float64 results agree with the reference to a
 // few ulps (exp() differs from glibc by <= 1 ulp).
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.cuh"
@@ -73,6 +74,8 @@ __device__ __forceinline__ void vstore(T* p, const T (&in)[W]) {
   for (int w = 0; w < W; ++w) q[w] = in[w];
   *reinterpret_cast<VT*>(p) = v;
 }
+
+#include "gat_fast.cuh"
 
 // kernels.hpp:385-423 node_scores: one thread per (node, head), sequential dot
 template <class T>
@@ -536,6 +539,47 @@ static int rows_grid(sgnn_ctx ctx, int32_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), (int64_t)ctx->num_sms * 32));
 }
 
+// Fast-path eligibility (gat_fast.cuh): returns R (vectors per lane) or 0.
+template <class T>
+static int fast_R(int32_t h, int32_t k) {
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  if (getenv("SGNN_GAT_GENERIC")) return 0;
+  if (h > gf::HF || k % VW != 0) return 0;
+  const int lph = k / VW, fv = h * k / VW;
+  const bool pow2 = (lph & (lph - 1)) == 0;
+  if (!((pow2 && lph <= 32) || lph % 32 == 0)) return 0;
+  const int R = pick_r(fv);
+  if (R > 8) return 0;
+  if (lph > 32 && R % (lph / 32) != 0) return 0;
+  return R;
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <class T>
+static int wgrid(int32_t n) {
+  constexpr int wpb = gf::WPB<T>::v;
+  return (int)std::max<int64_t>(1, ceil_div(n, wpb));
+}
+
+#define R_SWITCH(R, ...)                  \
+  switch (R) {                            \
+    case 1: { constexpr int RR = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int RR = 2; __VA_ARGS__; } break; \
+    case 4: { constexpr int RR = 4; __VA_ARGS__; } break; \
+    default: { constexpr int RR = 8; __VA_ARGS__; } break; \
+  }
+
+template <class T>
+static void node_scores_fast(sgnn_ctx ctx, int R, int32_t n, int32_t h, int32_t k, const T* M,
+                             const T* a_src, const T* a_dst, T* s, T* d) {
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  constexpr int wpb = gf::WPB<T>::v;
+  R_SWITCH(R, (gf::k_node_scores_fast<T, VW, RR><<<wgrid<T>(n), 32 * wpb, 0, ctx->stream>>>(
+                  n, h, k, M, a_src, a_dst, s, d)));
+  launched(ctx);
+}
+
 template <class T>
 void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T* theta,
                    const T* a_src, const T* a_dst, const T* bias, int32_t h, int32_t k,
@@ -547,15 +591,33 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
   DevBuf M((size_t)n * hk * sizeof(T), st), s((size_t)n * h * sizeof(T) + 8, st),
       d((size_t)n * h * sizeof(T) + 8, st), alpha, mask;
   gemm<T>(ctx, X, n, m, theta, m, hk, false, false, M.as<T>());
-  node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
   const int32_t* rp = p->rowptr.as<int32_t>();
   const int32_t* ci = p->cols.as<int32_t>();
-  if (level == SGNN_GAT_FULL) {
+  const int R = fast_R<T>(h, k);
+  if (R && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
+    constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+    constexpr int wpb = gf::WPB<T>::v;
+    node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+    if (level == SGNN_GAT_FULL) {
+      alpha = DevBuf((size_t)q * h * sizeof(T) + 8, st);
+      mask = DevBuf((size_t)q * h + 8, st);
+      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+                      n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias, out,
+                      alpha.as<T>(), mask.as<uint8_t>())));
+    } else {
+      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+                      n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias, out,
+                      (T*)nullptr, (uint8_t*)nullptr)));
+    }
+    launched(ctx);
+  } else if (level == SGNN_GAT_FULL) {
+    node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
     alpha = DevBuf((size_t)q * h * sizeof(T) + 8, st);
     mask = DevBuf((size_t)q * h + 8, st);
     launch_fwd<T, true, true>(ctx, n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias,
                               out, alpha.as<T>(), mask.as<uint8_t>());
   } else {
+    node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
     launch_fwd<T, false, true>(ctx, n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta,
                                bias, out, nullptr, nullptr);
   }
@@ -601,7 +663,12 @@ static void recompute(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* t
   } else {
     r.s = DevBuf((size_t)n * h * sizeof(T) + 8, st);
     r.d = DevBuf((size_t)n * h * sizeof(T) + 8, st);
-    node_scores<T>(ctx, n, h, k, r.Mp, a_src, a_dst, r.s.template as<T>(), r.d.template as<T>());
+    const int R = fast_R<T>(h, k);
+    if (R && al16(r.Mp) && al16(a_src) && al16(a_dst))
+      node_scores_fast<T>(ctx, R, n, h, k, r.Mp, a_src, a_dst, r.s.template as<T>(),
+                          r.d.template as<T>());
+    else
+      node_scores<T>(ctx, n, h, k, r.Mp, a_src, a_dst, r.s.template as<T>(), r.d.template as<T>());
     r.sp = r.s.template as<T>();
     r.dp = r.d.template as<T>();
   }
@@ -627,6 +694,45 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     mask_t = DevBuf((size_t)q * h + 8, st);
   }
   const T* alpha = cached ? c->alpha.as<T>() : alpha_t.as<T>();
+  {
+    const int R = fast_R<T>(h, k);
+    if (R && al16(G) && al16(r.Mp) && al16(dM.get()) && al16(a_src) && al16(a_dst)) {
+      constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+      constexpr int wpb = gf::WPB<T>::v;
+      const int32_t* rp = p->rowptr.as<int32_t>();
+      const int32_t* ci = p->cols.as<int32_t>();
+      if (cached) {
+        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+                        n, rp, ci, r.Mp, r.sp, r.dp, G, h, k, beta, c->alpha.as<T>(),
+                        c->mask.as<uint8_t>(), (T*)nullptr, da.as<T>(), dy.as<T>(), dS.as<T>())));
+      } else {
+        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+                        n, rp, ci, r.Mp, r.sp, r.dp, G, h, k, beta, (const T*)nullptr,
+                        (const uint8_t*)nullptr, alpha_t.as<T>(), da.as<T>(), dy.as<T>(),
+                        dS.as<T>())));
+      }
+      launched(ctx);
+      const int cgrid = (int)std::max<int64_t>(
+          1, std::min<int64_t>(ceil_div(n, wpb), (int64_t)ctx->num_sms * (32 / wpb)));
+      const int64_t nw = (int64_t)cgrid * wpb;
+      DevBuf psrc((size_t)nw * hk * 8, st), pdst((size_t)nw * hk * 8, st);
+      R_SWITCH(R, (gf::k_gat_bwd_col_fast<T, VW, RR><<<cgrid, 32 * wpb, 0, st>>>(
+                      n, p->colptr.as<int32_t>(), p->rows.as<int32_t>(), p->perm.as<int32_t>(),
+                      G, r.Mp, alpha, dy.as<T>(), dS.as<T>(), a_src, a_dst, h, k, dD.as<T>(),
+                      dM.as<T>(), psrc.as<double>(), pdst.as<double>())));
+      launched(ctx);
+      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>((int32_t)nw, hk,
+                                                                        psrc.as<double>(), d_a_src);
+      launched(ctx);
+      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>((int32_t)nw, hk,
+                                                                        pdst.as<double>(), d_a_dst);
+      launched(ctx);
+      gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
+              d_theta);
+      if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+      return;
+    }
+  }
   const int32_t* rp = p->rowptr.as<int32_t>();
   const int32_t* ci = p->cols.as<int32_t>();
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;

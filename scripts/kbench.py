@@ -30,7 +30,7 @@ def t(fn, iters=20):
     return statistics.median(ms) * 1e3
 
 which = sys.argv[1:] or ["nn", "tn", "nt", "colsum"]
-if any(w.startswith("spmm") for w in which):
+if any(w.startswith("spmm") or w.startswith("gat") for w in which):
     src, dst = d.synthetic_graph(n, 1166243 / n, 1)
     A = d.Adjacency.gcn_operator(n, src, dst, torch.float32, "csc")
 for w in which:
@@ -48,6 +48,18 @@ for w in which:
         us = t(lambda: A.spmm(X, transposed=True, out=outm)); byt = 4 * (n + 1) + 8 * A.nnz + 8 * n * m
     elif w == "spmm256":
         us = t(lambda: A.spmm(G, out=out)); byt = 4 * (n + 1) + 8 * A.nnz + 8 * n * k
+    elif w in ("gat", "gatfwd"):
+        if "P" not in globals():
+            P = d.Pattern.gat_pattern(n, src, dst)
+            thg, asg, adg, bg = d.gat_params(m, 8, 32, 14)
+            Gg = torch.randn(n, 256, device=dev)
+        def gstep(bwd=(w == "gat")):
+            o, c = d.gat_forward(P, X, thg, asg, adg, bg, 8, 0.2, "full")
+            if bwd:
+                d.gat_backward(P, Gg, thg, asg, adg, c, True)
+        us = t(gstep); byt = 0
     elif w == "copy":
         us = t(lambda: out.copy_(G)); byt = 8 * n * k
     print(f"{w}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s", flush=True)
+    if os.environ.get("ONE"):
+        break
