@@ -544,7 +544,7 @@ template <class T>
 static int fast_R(int32_t h, int32_t k) {
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;
   if (getenv("SGNN_GAT_GENERIC")) return 0;
-  if (h > gf::HF || k % VW != 0) return 0;
+  if (h > 8 || k % VW != 0) return 0;  // kernels instantiated for h <= 8
   const int lph = k / VW, fv = h * k / VW;
   const bool pow2 = (lph & (lph - 1)) == 0;
   if (!((pow2 && lph <= 32) || lph % 32 == 0)) return 0;
@@ -601,11 +601,11 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
     if (level == SGNN_GAT_FULL) {
       alpha = DevBuf((size_t)q * h * sizeof(T) + 8, st);
       mask = DevBuf((size_t)q * h + 8, st);
-      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, 8, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
                       n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias, out,
                       alpha.as<T>(), mask.as<uint8_t>())));
     } else {
-      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+      R_SWITCH(R, (gf::k_gat_fwd_fast<T, VW, RR, 8, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
                       n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta, bias, out,
                       (T*)nullptr, (uint8_t*)nullptr)));
     }
@@ -702,29 +702,32 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
       const int32_t* rp = p->rowptr.as<int32_t>();
       const int32_t* ci = p->cols.as<int32_t>();
       if (cached) {
-        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, 8, true><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
                         n, rp, ci, r.Mp, r.sp, r.dp, G, h, k, beta, c->alpha.as<T>(),
                         c->mask.as<uint8_t>(), (T*)nullptr, da.as<T>(), dy.as<T>(), dS.as<T>())));
       } else {
-        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
+        R_SWITCH(R, (gf::k_gat_bwd_row_fast<T, VW, RR, 8, false><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
                         n, rp, ci, r.Mp, r.sp, r.dp, G, h, k, beta, (const T*)nullptr,
                         (const uint8_t*)nullptr, alpha_t.as<T>(), da.as<T>(), dy.as<T>(),
                         dS.as<T>())));
       }
       launched(ctx);
-      const int cgrid = (int)std::max<int64_t>(
-          1, std::min<int64_t>(ceil_div(n, wpb), (int64_t)ctx->num_sms * (32 / wpb)));
-      const int64_t nw = (int64_t)cgrid * wpb;
-      DevBuf psrc((size_t)nw * hk * 8, st), pdst((size_t)nw * hk * 8, st);
-      R_SWITCH(R, (gf::k_gat_bwd_col_fast<T, VW, RR><<<cgrid, 32 * wpb, 0, st>>>(
+      R_SWITCH(R, (gf::k_gat_bwd_col_fast<T, VW, RR><<<wgrid<T>(n), 32 * wpb, 0, st>>>(
                       n, p->colptr.as<int32_t>(), p->rows.as<int32_t>(), p->perm.as<int32_t>(),
-                      G, r.Mp, alpha, dy.as<T>(), dS.as<T>(), a_src, a_dst, h, k, dD.as<T>(),
-                      dM.as<T>(), psrc.as<double>(), pdst.as<double>())));
+                      G, alpha, dy.as<T>(), dS.as<T>(), a_src, a_dst, h, k, dD.as<T>(),
+                      dM.as<T>())));
       launched(ctx);
-      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>((int32_t)nw, hk,
+      // attention-parameter gradients: one pass over M for a_src and a_dst
+      const int32_t chunk = (int32_t)std::max<int64_t>(64, ceil_div(n, ctx->num_sms * 4));
+      const int32_t nch = (int32_t)std::max<int64_t>(1, ceil_div(n, chunk));
+      DevBuf psrc((size_t)nch * hk * 8, st), pdst((size_t)nch * hk * 8, st);
+      gf::k_attgrad2_partial<T, VW><<<nch, 256, 0, st>>>(n, h, k, r.Mp, dS.as<T>(), dD.as<T>(), chunk,
+                                                    psrc.as<double>(), pdst.as<double>());
+      launched(ctx);
+      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
                                                                         psrc.as<double>(), d_a_src);
       launched(ctx);
-      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>((int32_t)nw, hk,
+      gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
                                                                         pdst.as<double>(), d_a_dst);
       launched(ctx);
       gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
