@@ -53,6 +53,24 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+# component of the step -> kernel name in the committed ncu capture
+_KERNEL_OF = {"spmm_fwd_f128": "k_spmm_lean<1, 2>", "spmm_bwd_f128": "k_spmm_lean<1, 2>",
+              "gemm_PxTheta": "tc::k_gemm_tc<0, 0, 128, 1>",
+              "gemm_GThetaT": "tc::k_gemm_tc<0, 1, 128, 1>",
+              "colsum_db": "k_colsum_partial<float>"}
+
+
+def _traffic(component):
+    """DRAM bytes per launch of the component's kernel from the committed
+    `ncu --set full` capture (profiles/traffic.json, scripts/summarize_profiles.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+        return int(t["kernels"][_KERNEL_OF[component]] * 1e6)
+    except Exception:
+        return None
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -261,7 +279,7 @@ def run_ours(args):
     spmm_gbs = spmm_bytes / (comps["spmm_fwd_f128"] * 1e-3) / 1e9
     roofline = {"kernel": dominant, "bound": "hbm", "achieved": round(achieved, 1),
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": None, "algorithmic_bytes": dom_bytes, "peak_source": peak_kind,
+                "traffic": _traffic(dominant), "algorithmic_bytes": dom_bytes, "peak_source": peak_kind,
                 "ms": round(comps[dominant], 4)}
 
     # ---- GAT layer (h=8, k=32, cache level full) on the same graph ----------
@@ -340,6 +358,81 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_ours_dist(args):
+    """N > 1 (torchrun, one rank per GPU): the 1-D destination-row partitioned
+    GCN layer of paper_2308_12093_b200.dist over NCCL (all-gather of the
+    propagated operand, all-reduce of dTheta / db).  The graph is fixed, so
+    the scaling is strong; value = max-over-ranks ms per fwd+bwd step."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2308_12093_b200 import device as d
+    from paper_2308_12093_b200 import dist as pd
+
+    ctx = d.Context.default(local)
+    dev = ctx.device
+    stream = torch.cuda.current_stream(dev)
+    src, dst = d.synthetic_graph(ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED)
+    ones = torch.ones(src.numel(), dtype=torch.float32, device=dev)
+    r, c, v = d.canonicalize(ARXIV_N, ARXIV_N, src, dst, ones, ctx)
+    r, c, v = d.gcn_normalize(ARXIV_N, r, c, v, ctx)
+    layer = pd.DistGcnLayer(ARXIV_N, r.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(),
+                            pd.DeviceOps(dev), torch.float32)
+    r0, r1 = layer.r0, layer.r1
+    X = d.random_uniform(ARXIV_N, M_IN, SEED + 11, ctx=ctx)[r0:r1].contiguous()
+    G = d.random_uniform(ARXIV_N, K_OUT, SEED + 12, ctx=ctx)[r0:r1].contiguous()
+    theta, bias = d.gcn_params(M_IN, K_OUT, SEED + 13, ctx=ctx)
+    s = d.resolve_scheme("adaptive", M_IN, K_OUT, True, True)
+    scheme = (s.forward, s.backward, s.caching)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        out, cache = layer.forward(X, theta, bias, scheme)
+        return layer.backward(G, theta, cache, True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            flush.view(torch.int64).sum()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(ms) / len(ms)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mean_ms = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (reference generators, device-side)",
+            "config": dict(_config(), scheme=str(s), nnz=int(r.numel()),
+                           parallelism=f"row-partition x{world} (NCCL all-gather/all-reduce)"),
+            "clocks": clk.summary(),
+            "edges_per_s": round(int(r.numel()) / (mean_ms * 1e-3), 1),
+            "rows_per_rank": [layer.bounds[p + 1] - layer.bounds[p] for p in range(world)],
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -348,11 +441,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the row-partitioned multi-GPU path even at WORLD_SIZE=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference_arm(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
+        run_ours_dist(args)
     else:
         run_ours(args)
 
