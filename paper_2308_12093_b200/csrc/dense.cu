@@ -153,14 +153,15 @@ template void gemm_simt<double>(sgnn_ctx, const double*, int32_t, int32_t, const
 
 // tcgen05 path (gemm_tc.cu); returns false when the shape is not supported
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
-                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias);
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
+                 float* colsum_b);
 
 template <>
 void gemm<float>(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias) {
   const int32_t kk = ta ? ra : ca, kb = tb ? cb : rb;
   require(kk == kb, "gemm: inner dimensions do not match");
-  if (gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias)) return;
+  if (gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, nullptr)) return;
   gemm_simt<float>(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias);
 }
 template <>
@@ -237,6 +238,24 @@ void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out) {
   launched(ctx);
 }
 template void column_sums<float>(sgnn_ctx, const float*, int32_t, int32_t, float*);
+
+// C = A^T B and colsum_b = 1^T B (dTheta and d_bias of one backward: B = dX'
+// is read once when the tcgen05 kernel can fuse the column sums)
+template <>
+void gemm_tn_colsum<float>(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                           int32_t rb, int32_t cb, float* C, float* colsum_b) {
+  require(ra == rb, "gemm: inner dimensions do not match");
+  if (gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, true, false, C, nullptr, colsum_b)) return;
+  column_sums<float>(ctx, B, rb, cb, colsum_b);
+  gemm<float>(ctx, A, ra, ca, B, rb, cb, true, false, C);
+}
+template <>
+void gemm_tn_colsum<double>(sgnn_ctx ctx, const double* A, int32_t ra, int32_t ca,
+                            const double* B, int32_t rb, int32_t cb, double* C,
+                            double* colsum_b) {
+  column_sums<double>(ctx, B, rb, cb, colsum_b);
+  gemm<double>(ctx, A, ra, ca, B, rb, cb, true, false, C);
+}
 template void column_sums<double>(sgnn_ctx, const double*, int32_t, int32_t, double*);
 
 // ---------------------------------------------------------------------------

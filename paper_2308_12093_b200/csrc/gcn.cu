@@ -50,11 +50,11 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
   const int32_t* cp = A->colptr.as<int32_t>();
   const int32_t* cr = A->crows.as<int32_t>();
   const T* cv = A->cvals.as<T>();
-  column_sums<T>(ctx, G, n, k, d_bias);
   switch (c->scheme.backward) {
     case SGNN_FUSED_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf S((size_t)n * k * sizeof(T), st);
+      column_sums<T>(ctx, G, n, k, d_bias);
       spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz);
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
       if (fg) gemm<T>(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input);
@@ -64,7 +64,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf P((size_t)n * m * sizeof(T), st);
       spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
-      gemm<T>(ctx, P.as<T>(), n, m, G, n, k, true, false, d_theta);
+      gemm_tn_colsum<T>(ctx, P.as<T>(), n, m, G, n, k, d_theta, d_bias);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
@@ -74,7 +74,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     }
     case SGNN_SPLIT_PROPAGATE_CACHED: {
       const T* P = c->saved_propagated.as<T>();
-      gemm<T>(ctx, P, n, m, G, n, k, true, false, d_theta);
+      gemm_tn_colsum<T>(ctx, P, n, m, G, n, k, d_theta, d_bias);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());

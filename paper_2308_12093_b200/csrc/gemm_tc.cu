@@ -70,6 +70,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // UMMA shared-memory descriptor, version 1.  Layout type 2 = SWIZZLE_128B
 // (16-byte chunks, K-major tiles); 1 = SWIZZLE_128B_BASE32B (32-byte chunks,
 // 4-row period) -- the only layout UMMA accepts for MN-major tf32 operands.
@@ -185,7 +194,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A raw | B hi | B lo
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES >= 4 ? 4 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 x (32 x 32 fp32)
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int NA = 2;                                // TMEM A buffers (hi|lo, 64 cols)
   static constexpr uint32_t USED = 2 * BN + NA * 64;          // accumulators + A buffers
   static constexpr uint32_t TMEM_COLS = USED <= 256 ? 256 : 512;
@@ -206,16 +216,18 @@ struct Cfg {
 template <bool A_MN, bool B_MN, int BN, bool B_PRE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kchunk,
-              int splits, float* __restrict__ C, int ldc, const float* __restrict__ bias,
-              float* __restrict__ part) {
+              const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
+              int M, int N, int K, int kchunk, int splits, float* __restrict__ C, int ldc,
+              const float* __restrict__ bias, float* __restrict__ part, int tma_store,
+              float* __restrict__ cs_part) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
   constexpr int NA = CF::NA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
+  uint8_t* epi = smem + S * CF::STAGE_BYTES;  // 1024-aligned (STAGE_BYTES % 1024 == 0)
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + CF::EPI_BYTES);
   uint64_t* empty = full + S;
   uint64_t* afull = empty + S;    // [NA] converters -> MMA
   uint64_t* aempty = afull + NA;  // [NA] MMA -> converters
@@ -346,16 +358,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int r = q * 32 + lane;  // tile row == TMEM lane
     const int ctid = threadIdx.x - 64;
+    // column sums of an MN-major B over K (d_bias = 1^T dX' fused into
+    // dTheta = P^T dX'): thread ctid always sees the same 4 columns of every
+    // 32-column box of a stage (chunk i = ctid + 128 j -> box j/2, K-row
+    // ctid/8 + 16 (j&1), 32 B atom ((ctid&7)>>1) ^ ((ctid>>3)&3), see split_tile)
+    constexpr int NB = BN / 32;
+    const bool want_cs = (cs_part != nullptr) && B_MN && !B_PRE;
+    float cs[NB][4];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) cs[b][0] = cs[b][1] = cs[b][2] = cs[b][3] = 0.f;
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int z, m0, n0, kb, nk;
       tile_of(t, z, m0, n0, kb, nk);
+      const bool cs_tile = want_cs && m0 == 0;
       for (int ks = 0; ks < nk; ++ks, ++it) {
         const int s = it % S, a = it % NA;
         mbar_wait(&full[s], (it / S) & 1);
         if (!B_PRE) {
-          split_tile(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
-                     CF::B_BYTES / 16, ctid, 128);
+          if (B_MN && cs_tile) {
+            float4* raw = reinterpret_cast<float4*>(b_hi(s));
+            float4* lo = reinterpret_cast<float4*>(b_lo(s));
+#pragma unroll
+            for (int j = 0; j < CF::B_BYTES / 16 / 128; ++j) {
+              const int i = ctid + 128 * j;
+              float4 v = raw[i];
+              cs[j >> 1][0] += v.x;
+              cs[j >> 1][1] += v.y;
+              cs[j >> 1][2] += v.z;
+              cs[j >> 1][3] += v.w;
+              float4 h, l;
+              h.x = __uint_as_float(tf32_hi(v.x));
+              h.y = __uint_as_float(tf32_hi(v.y));
+              h.z = __uint_as_float(tf32_hi(v.z));
+              h.w = __uint_as_float(tf32_hi(v.w));
+              l.x = __fsub_rn(v.x, h.x);
+              l.y = __fsub_rn(v.y, h.y);
+              l.z = __fsub_rn(v.z, h.z);
+              l.w = __fsub_rn(v.w, h.w);
+              raw[i] = h;
+              lo[i] = l;
+            }
+          } else {
+            split_tile(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
+                       CF::B_BYTES / 16, ctid, 128);
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         float v[32];
@@ -395,12 +442,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
       }
+      if (cs_tile) {
+        // combine the 4 lanes holding the same logical 32 B atom (fixed order),
+        // one lane per atom writes this warp's partial: cs_part[z][warp][n]
+        const int half = lane & 1, kr3 = (lane >> 3) & 3;
+        const int c32 = ((lane & 7) >> 1) ^ kr3;
+        float* dst = cs_part + ((int64_t)z * 4 + q) * N;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float sum = 0.f;
+#pragma unroll
+            for (int r3 = 0; r3 < 4; ++r3) {
+              const int src = ((((c32 ^ r3) << 1) | half)) + 8 * r3;
+              sum += __shfl_sync(0xffffffffu, cs[b][e], src);
+            }
+            cs[b][e] = 0.f;
+            const int n = n0 + b * 32 + c32 * 8 + half * 4 + e;
+            if (kr3 == 0 && n < N) dst[n] = sum;
+          }
+        }
+      }
     }
   } else {
     // ---------------- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 ----------------
     const int q = warp & 3;
     const bool vec = ((ldc & 3) == 0) && ((N & 3) == 0);
-    int tl = 0;
+    int tl = 0, ecnt = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
       int z, m0, n0, kb, nk;
       tile_of(t, z, m0, n0, kb, nk);
@@ -412,6 +481,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
+        if (tma_store) {
+          // stage the 32 x 32 block in smem (SWIZZLE_128B: 16 B chunk j of row
+          // `lane` at chunk j ^ (lane & 7), conflict-free) and let TMA write
+          // full 128 B row segments (clipped at M, N)
+          uint8_t* buf = epi + q * 8192 + (ecnt & 1) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          const int col0 = n0 + c;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            if (bias && col0 + 4 * j < N) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0 + 4 * j));
+              v.x = __fadd_rn(v.x, b.x);
+              v.y = __fadd_rn(v.y, b.y);
+              v.z = __fadd_rn(v.z, b.z);
+              v.w = __fadd_rn(v.w, b.w);
+            }
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tmC, buf, col0, m0 + q * 32);
+          ++ecnt;
+          continue;
+        }
         if (row >= M) continue;
         const int col0 = n0 + c;
         float* dst = part ? part + ((int64_t)z * M + row) * N : C + (int64_t)row * ldc;
@@ -441,6 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[abuf]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -451,17 +548,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-__global__ void k_reduce_splits(int splits, int64_t MN, int N, const float* __restrict__ part,
-                                float* __restrict__ C, int ldc, const float* __restrict__ bias) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < MN;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += (double)part[(int64_t)z * MN + x];
+// C = sum over split partials (+ bias).  Block = 32 consecutive outputs x 8
+// split groups; each thread folds every 8th split in float64, then a fixed
+// smem tree -- deterministic, and 8x the memory parallelism of one thread per
+// output (the split count is ~num_sms / tiles, ~74 for dTheta).
+__global__ void __launch_bounds__(256) k_reduce_splits(int splits, int64_t MN, int N,
+                                                       const float* __restrict__ part,
+                                                       float* __restrict__ C, int ldc,
+                                                       const float* __restrict__ bias) {
+  __shared__ double sh[8][33];
+  const int g = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t x = blockIdx.x * 32LL + l;
+  double s = 0.0;
+  if (x < MN) {
+#pragma unroll 4
+    for (int z = g; z < splits; z += 8) s += (double)part[(int64_t)z * MN + x];
+  }
+  sh[g][l] = s;
+  __syncthreads();
+  if (g == 0 && x < MN) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sh[k][l];
     const int64_t row = x / N, col = x % N;
-    float v = (float)s;
+    float v = (float)t;
     if (bias) v = __fadd_rn(v, bias[col]);
     C[row * ldc + col] = v;
   }
+}
+
+// out[n] = sum over z, warp of the converters' column-sum partials
+__global__ void k_colsum_parts(int parts, int N, const float* __restrict__ cs_part,
+                               float* __restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int p = 0; p < parts; ++p) s += (double)cs_part[(int64_t)p * N + n];
+  out[n] = (float)s;
 }
 
 // ---- host side -------------------------------------------------------------
@@ -496,10 +619,13 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t o
   return r == CUDA_SUCCESS;
 }
 
+struct Maps {
+  CUtensorMap a, b, blo, c;
+};
+
 template <bool A_MN, bool B_MN, int BN, bool B_PRE>
-static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb,
-                   const CUtensorMap& mbl, int M, int N, int K, int splits, int kchunk, float* C,
-                   const float* bias, float* part) {
+static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits, int kchunk,
+                   float* C, const float* bias, float* part, int tma_store, float* cs_part) {
   auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE>;
   const int smem = Cfg<BN>::SMEM;
   static bool attr_set = false;  // per instantiation
@@ -509,17 +635,17 @@ static void launch(sgnn_ctx ctx, const CUtensorMap& ma, const CUtensorMap& mb,
   }
   const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * splits;
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
-  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(ma, mb, mbl, M, N, K, kchunk, splits, C, N,
-                                                  bias, part);
+  kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(mp.a, mp.b, mp.blo, mp.c, M, N, K, kchunk,
+                                                  splits, C, N, bias, part, tma_store, cs_part);
   launched(ctx);
 }
 
 template <int BN>
-static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const CUtensorMap& ma,
-                     const CUtensorMap& mb, const CUtensorMap& mbl, int M, int N, int K,
-                     int splits, int kchunk, float* C, const float* bias, float* part) {
+static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& mp, int M, int N,
+                     int K, int splits, int kchunk, float* C, const float* bias, float* part,
+                     int tma_store, float* cs_part) {
 #define L(AM, BM_, PR) \
-  launch<AM, BM_, BN, PR>(ctx, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, part)
+  launch<AM, BM_, BN, PR>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part)
   if (pre) {
     if (a_mn && b_mn) L(true, true, true);
     else if (a_mn) L(true, false, true);
@@ -546,9 +672,14 @@ static bool tc_disabled() {
 }
 
 // Returns false (caller falls back to the SIMT kernel) when the shape or the
-// operand alignment does not fit the TMA/UMMA path.
+// operand alignment does not fit the TMA/UMMA path.  colsum_b (optional, only
+// for C = A^T B with B read MN-major and split in the kernel): also writes the
+// column sums of B over its K rows -- d_bias = 1^T dX' fused into the dTheta
+// GEMM, so dX' is read once.  Returns false without doing anything if the
+// fused form does not apply (the caller then runs the two ops separately).
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
-                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias) {
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
+                 float* colsum_b) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
@@ -564,26 +695,26 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   // the kernel streams both halves with TMA and spends no smem bandwidth on it.
   const int64_t belems = (int64_t)rb * cb;
   const bool pre = belems * 8 <= (int64_t)ra * ca;
+  if (colsum_b && (pre || !b_mn)) return false;
   DevBuf bsplit;
   const float* Bhi = B;
   const float* Blo = B;
+  Maps mp;
+  // A: ta -> stored K x M (MN-major), else M x K (K-major)
+  const bool okA = a_mn ? make_map(&mp.a, A, M, K, ca, BK, true)
+                        : make_map(&mp.a, A, K, M, ca, BM, false);
+  if (!okA) return false;
   if (pre) {
     bsplit = DevBuf((size_t)belems * 8, ctx->stream);
-    k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
-        belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);
-    launched(ctx);
     Bhi = bsplit.as<float>();
     Blo = bsplit.as<float>() + belems;
   }
-  CUtensorMap ma, mb, mbl;
-  // A: ta -> stored K x M (MN-major), else M x K (K-major)
-  const bool okA =
-      a_mn ? make_map(&ma, A, M, K, ca, BK, true) : make_map(&ma, A, K, M, ca, BM, false);
   // B: tb -> stored N x K (K-major), else K x N (MN-major)
-  bool okB = b_mn ? make_map(&mb, Bhi, N, K, cb, BK, true) : make_map(&mb, Bhi, K, N, cb, BN, false);
-  okB = okB && (b_mn ? make_map(&mbl, Blo, N, K, cb, BK, true)
-                     : make_map(&mbl, Blo, K, N, cb, BN, false));
-  if (!okA || !okB) return false;
+  bool okB = b_mn ? make_map(&mp.b, Bhi, N, K, cb, BK, true)
+                  : make_map(&mp.b, Bhi, K, N, cb, BN, false);
+  okB = okB && (b_mn ? make_map(&mp.blo, Blo, N, K, cb, BK, true)
+                     : make_map(&mp.blo, Blo, K, N, cb, BN, false));
+  if (!okB) return false;
   const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
   int splits = 1;
   const int ksteps = (int)ceil_div(K, BK);
@@ -593,21 +724,39 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   }
   const int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
   splits = (int)ceil_div(K, kchunk);
-  DevBuf part;
+  // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
+  const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));
+  if (!tma_store) mp.c = mp.a;  // unused
+  if (pre) {
+    k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
+        belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);
+    launched(ctx);
+  }
+  DevBuf part, csp;
   float* pp = nullptr;
   if (splits > 1) {
     part = DevBuf((size_t)splits * M * N * sizeof(float), ctx->stream);
     pp = part.as<float>();
   }
+  float* cs = nullptr;
+  if (colsum_b) {
+    csp = DevBuf((size_t)splits * 4 * N * sizeof(float), ctx->stream);
+    cs = csp.as<float>();
+  }
   switch (BN) {
-    case 32: dispatch<32>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
-    case 64: dispatch<64>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
-    default: dispatch<128>(ctx, a_mn, b_mn, pre, ma, mb, mbl, M, N, K, splits, kchunk, C, bias, pp); break;
+    case 32: dispatch<32>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
+    case 64: dispatch<64>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
+    default: dispatch<128>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
   }
   if (splits > 1) {
     const int64_t MN = (int64_t)M * N;
-    k_reduce_splits<<<grid_for(ctx, MN, 256), 256, 0, ctx->stream>>>(splits, MN, N, pp, C, N,
-                                                                     bias);
+    k_reduce_splits<<<(unsigned)ceil_div(MN, 32), 256, 0, ctx->stream>>>(splits, MN, N, pp, C, N,
+                                                                         bias);
+    launched(ctx);
+  }
+  if (colsum_b) {
+    k_colsum_parts<<<(unsigned)ceil_div(N, 128), 128, 0, ctx->stream>>>(splits * 4, N, cs,
+                                                                         colsum_b);
     launched(ctx);
   }
   return true;

@@ -64,6 +64,9 @@ void gemm(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int32_t 
 
 template <class T>
 void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out);
+template <class T>
+void gemm_tn_colsum(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int32_t rb,
+                    int32_t cb, T* C, T* colsum_b);
 
 template <class T>
 void random_uniform(sgnn_ctx ctx, int64_t count, uint64_t seed, double lo, double hi, T* out);

@@ -1,0 +1,84 @@
+"""Row-partitioned GCN layer on the GPU.
+
+* world_size 1 over NCCL: DistGcnLayer with the product backend (DeviceOps ->
+  libsgnn_cuda.so) against the oracle, every scheme.
+* virtual partitions on one GPU: the row blocks A'_p / A'^T_p that rank p
+  would own propagate bit-identically to the rows of the single-GPU product
+  (the accumulation order inside a row is unchanged by the partition)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scheme", [(0, 0, 0), (1, 1, 0), (2, 2, 1), (0, 1, 0), (1, 0, 0)])
+@pytest.mark.parametrize("fg", [False, True])
+def test_dist_layer_nccl_world1(nccl_world1, orc, scheme, fg):
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m, k = 3000, 48, 40
+    _, s, t = orc.synthetic_graph(n, 9.0, 5)
+    op = orc.gcn_operator(n, s, t)
+    X = orc.random_uniform(n, m, 11)
+    th, bi = orc.gcn_params(m, k, 13)
+    G = orc.random_uniform(n, k, 12)
+    ref = orc.gcn_layer(op, X, th, bi, scheme, G, fg)
+    layer = pd.DistGcnLayer(n, op.rows, op.cols, op.vals, pd.DeviceOps("cuda:0"), torch.float64)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    out, cache = layer.forward(cu(X), cu(th), cu(bi), scheme)
+    dth, db, dx = layer.backward(cu(G), cu(th), cache, fg)
+    assert orc.max_rel_diff(out.cpu().numpy(), ref[0]) < 1e-12
+    assert orc.max_rel_diff(dth.cpu().numpy(), ref[1]) < 1e-10
+    assert orc.max_rel_diff(db.cpu().numpy(), ref[2]) < 1e-12
+    if fg:
+        assert orc.max_rel_diff(dx.cpu().numpy(), ref[3]) < 1e-10
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_partition_blocks_bit_identical(orc, parts):
+    from paper_2308_12093_b200 import device as d
+    from paper_2308_12093_b200 import dist as pd
+
+    n, f = 20000, 128
+    _, s, t = orc.synthetic_graph(n, 13.77, 1)
+    op = orc.gcn_operator(n, s, t)
+    rowptr = np.concatenate([[0], np.cumsum(np.bincount(op.rows, minlength=n))])
+    bounds = pd.partition_rows(rowptr, parts)
+    ops = pd.DeviceOps("cuda:0")
+    cu = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa: E731
+    full = d.Adjacency(n, n, cu(op.rows, torch.int32), cu(op.cols, torch.int32),
+                       cu(op.vals, torch.float32), "csc")
+    B = d.random_uniform(n, f, 7)
+    ref = full.spmm(B)
+    refT = full.spmm(B, transposed=True)
+    for p in range(parts):
+        r0, r1 = bounds[p], bounds[p + 1]
+        rb = pd.row_block(op.rows, op.cols, op.vals.astype(np.float32), r0, r1)
+        A_p = ops.adjacency(r1 - r0, n, *rb, torch.float32)
+        assert torch.equal(A_p.spmm(B), ref[r0:r1])
+        tb = pd.transposed_block(op.rows, op.cols, op.vals.astype(np.float32), r0, r1)
+        AT_p = ops.adjacency(r1 - r0, n, *tb, torch.float32)
+        assert torch.equal(AT_p.spmm(B), refT[r0:r1])
