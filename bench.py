@@ -11,8 +11,10 @@ device with the reference's counter-based RNG (bit-identical values).
 
   value        device time per fwd+bwd step, inputs resident in HBM, L2 flushed
                (256 MiB write) before every timed step, CUDA events on the stream
-  e2e          the same step through the public API with HOST buffers: pinned
-               H2D of X and dX', D2H of out, dTheta, db, dX inside the timed region
+  e2e          the same step through the public API with HOST buffers
+               (sgnn_gcn_step_host): pinned H2D of X and dX', D2H of out, dTheta,
+               db, dX inside the timed region, overlapped with compute and with
+               each other on copy streams
   roofline     dominant kernel of the step, timed live here in isolation
   cpu_baseline the reference itself (oracle/_ref, compiled from the unmodified
                headers, OpenMP on every host core) on the same workload
@@ -304,14 +306,9 @@ def run_ours(args):
     h_dx = torch.empty((n, M_IN), dtype=torch.float32, pin_memory=True)
 
     def e2e_step():
-        Xd = hX.to(dev, non_blocking=True)
-        Gd = hG.to(dev, non_blocking=True)
-        out, cache = d.gcn_forward(A, Xd, theta, bias, scheme)
-        dth, db, dx = d.gcn_backward(A, Gd, theta, cache, True)
-        h_out.copy_(out, non_blocking=True)
-        h_dth.copy_(dth, non_blocking=True)
-        h_db.copy_(db, non_blocking=True)
-        h_dx.copy_(dx, non_blocking=True)
+        # public host-buffer step (sgnn_gcn_step_host): pinned H2D of X and dX',
+        # D2H of out, dTheta, db, dX, overlapped with compute on copy streams
+        d.gcn_step_host(A, hX, theta, bias, scheme, hG, True, h_out, h_dth, h_db, h_dx)
 
     e2e_ms = statistics.mean(timed(e2e_step, max(3, args.steps), 2))
     h2d = hX.numel() * 4 + hG.numel() * 4

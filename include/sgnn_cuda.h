@@ -240,6 +240,26 @@ int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache cach
                                const void* theta, const void* a_src, const void* a_dst,
                                void* alpha_hq, uint8_t* mask_hq);
 
+/* ---- host-buffer layer steps (pipeline.cu) -------------------------------
+ * One forward + backward step with HOST inputs and outputs, the shape of the
+ * reference API (DenseMatrix in host memory, gcn.hpp:91-193 / gat.hpp:89-219)
+ * and of its benchmark step (forward, then backward with a given output
+ * gradient, bench.hpp:193-219).  Parameters stay device-resident; X and the
+ * output gradient are copied in, the output and all gradients copied out.
+ * Transfers run on internal copy streams, overlapped with compute and with
+ * each other (output D2H while dX' is H2D).  Stream-ordered on the ctx
+ * stream; host buffers should be pinned for the copies to be asynchronous.
+ * h_d_input may be NULL when needs_feature_grad == 0. */
+int sgnn_gcn_step_host(sgnn_ctx ctx, sgnn_adj adj, const void* hX, int32_t m, const void* theta,
+                       const void* bias, int32_t k, const sgnn_scheme* scheme, const void* hG,
+                       int needs_feature_grad, void* h_out, void* h_d_theta, void* h_d_bias,
+                       void* h_d_input);
+int sgnn_gat_step_host(sgnn_ctx ctx, sgnn_pattern p, const void* hX, int32_t m,
+                       const void* theta, const void* a_src, const void* a_dst, const void* bias,
+                       int32_t heads, int32_t k, double beta, int level, int dtype,
+                       const void* hG, int needs_feature_grad, void* h_out, void* h_d_theta,
+                       void* h_d_a_src, void* h_d_a_dst, void* h_d_bias, void* h_d_input);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,10 @@ _SIGS = {
     "sgnn_gat_cache_destroy": (INT, [VP]),
     "sgnn_gat_cache_extra_bytes": (INT, [VP, PI64]),
     "sgnn_gat_cache_edge_values": (INT, [VP, VP, VP, VP, VP, VP, VP, VP]),
+    "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
+                                 VP, VP]),
+    "sgnn_gat_step_host": (INT, [VP, VP, VP, I32, VP, VP, VP, VP, I32, I32, D, INT, INT, VP, INT,
+                                 VP, VP, VP, VP, VP, VP]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

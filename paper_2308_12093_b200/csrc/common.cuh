@@ -53,6 +53,8 @@ void set_last_error(const std::string& s);
     return SGNN_ERUNTIME;                           \
   }
 
+struct Pipe;  // host-buffer step staging (pipeline.cu)
+
 }  // namespace sgnn
 
 struct sgnn_ctx_s {
@@ -61,6 +63,7 @@ struct sgnn_ctx_s {
   bool own_stream = false;
   int num_sms = 148;
   int64_t launches = 0;
+  sgnn::Pipe* pipe = nullptr;  // lazily created copy streams + staging buffers
 };
 
 namespace sgnn {

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace sgnn {
 static thread_local std::string g_last_error;
@@ -43,6 +44,10 @@ int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out) {
 int sgnn_ctx_destroy(sgnn_ctx ctx) {
   SGNN_API_BEGIN
   if (!ctx) return SGNN_OK;
+  if (ctx->pipe) {
+    cudaStreamSynchronize(ctx->stream);
+    destroy_pipe(ctx);
+  }
   if (ctx->own_stream) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);

@@ -50,6 +50,19 @@ struct sgnn_gat_cache_s {
 
 namespace sgnn {
 
+// Copy streams, events and reusable device staging buffers of the host-buffer
+// layer steps (pipeline.cu); owned by the context.
+struct Pipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev[8] = {};
+  void* ws[8] = {};
+  size_t cap[8] = {};
+  ~Pipe();
+  void* buf(int slot, size_t bytes);
+};
+Pipe& pipe(sgnn_ctx ctx);
+void destroy_pipe(sgnn_ctx ctx);
+
 void build_ptr(sgnn_ctx ctx, const int32_t* sorted_ids, int64_t nnz, int32_t n, int32_t* ptr);
 
 // C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)

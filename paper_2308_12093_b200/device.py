@@ -410,6 +410,53 @@ def gcn_backward(adj: Adjacency, d_out, theta, cache: GcnCache, needs_feature_gr
     return d_theta, d_bias, (d_input if needs_feature_grad else None)
 
 
+def _host(t, name):
+    if t.device.type != "cpu" or not t.is_contiguous():
+        raise ValueError(f"{name}: contiguous host tensor expected")
+    return t
+
+
+def gcn_step_host(adj: Adjacency, hX, theta, bias, scheme, hG, needs_feature_grad,
+                  h_out, h_d_theta, h_d_bias, h_d_input=None):
+    """One GCN forward+backward step from HOST buffers (pinned for async
+    copies): X and dX' in, out / dTheta / db / dX out; parameters on the
+    device.  Copies overlap compute and each other (pipeline.cu).  Stream-
+    ordered: synchronize the context before reading the host outputs."""
+    m, k = theta.shape
+    for t, nm in ((hX, "X"), (hG, "d_out"), (h_out, "out"), (h_d_theta, "d_theta"),
+                  (h_d_bias, "d_bias")):
+        _host(t, nm)
+    if hX.shape != (adj.n_rows, m) or hG.shape != (adj.n_rows, k):
+        raise ValueError("gcn_step_host: shape mismatch")
+    if needs_feature_grad:
+        _host(h_d_input, "d_input")
+    check(lib.sgnn_gcn_step_host(adj.ctx.handle, adj.handle, _p(hX), m, _p(theta.contiguous()),
+                                 _p(bias.contiguous()), k, C.byref(scheme), _p(hG),
+                                 int(bool(needs_feature_grad)), _p(h_out), _p(h_d_theta),
+                                 _p(h_d_bias), _p(h_d_input) if needs_feature_grad else None))
+
+
+def gat_step_host(pattern: Pattern, hX, theta, a_src, a_dst, bias, heads, beta, level, hG,
+                  needs_feature_grad, h_out, h_d_theta, h_d_a_src, h_d_a_dst, h_d_bias,
+                  h_d_input=None):
+    """GAT counterpart of gcn_step_host (gat.hpp:89-219 from host buffers)."""
+    if isinstance(level, str):
+        level = _c.LEVELS[level]
+    m, hk = theta.shape
+    k = hk // heads
+    for t, nm in ((hX, "X"), (hG, "d_out"), (h_out, "out"), (h_d_theta, "d_theta")):
+        _host(t, nm)
+    if hX.shape != (pattern.n, m) or hG.shape != (pattern.n, hk):
+        raise ValueError("gat_step_host: shape mismatch")
+    check(lib.sgnn_gat_step_host(pattern.ctx.handle, pattern.handle, _p(hX), m,
+                                 _p(theta.contiguous()), _p(a_src.contiguous()),
+                                 _p(a_dst.contiguous()), _p(bias.contiguous()), heads, k,
+                                 float(beta), int(level), _dt(theta), _p(hG),
+                                 int(bool(needs_feature_grad)), _p(h_out), _p(h_d_theta),
+                                 _p(h_d_a_src), _p(h_d_a_dst), _p(h_d_bias),
+                                 _p(h_d_input) if needs_feature_grad else None))
+
+
 # ---- GAT layer (gat.hpp:89-219) ------------------------------------------------
 class GatCache:
     def __init__(self, handle, X, level, heads, k):

@@ -7,6 +7,7 @@ from paper_2308_12093_b200 import device as d
 
 n, m, k = 169343, 128, 256
 dev = torch.device("cuda")
+torch.manual_seed(0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 X = torch.randn(n, m, device=dev)
 G = torch.randn(n, k, device=dev)
@@ -58,6 +59,11 @@ for w in which:
             if bwd:
                 d.gat_backward(P, Gg, thg, asg, adg, c, True)
         us = t(gstep); byt = 0
+    elif w == "hash":  # bitwise fingerprint of the SpMM outputs (compare across modes)
+        A.spmm(X, out=outm); A.spmm(G, out=out); o3 = torch.empty_like(outm); A.spmm(X, transposed=True, out=o3)
+        torch.cuda.synchronize()
+        hs = [int(t.view(torch.int32).to(torch.int64).mul(torch.arange(t.numel(), device=dev).view(t.shape) % 1000003 + 1).sum()) for t in (outm, out, o3)]
+        print("hash", hs, flush=True); continue
     elif w == "copy":
         us = t(lambda: out.copy_(G)); byt = 8 * n * k
     print(f"{w}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s", flush=True)

@@ -181,3 +181,46 @@ def test_gat_rows_sum_to_one_and_single_node(d, orc):
     th1, as1, ad1, b1 = orc.gat_params(4, 2, 3, 4)
     out, _ = d.gat_forward(p1, cu(X1), cu(th1), cu(as1), cu(ad1), cu(b1), 2)
     assert orc.max_rel_diff(np_(out), X1 @ th1 + b1) < 1e-15
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("fg", [0, 1])
+def test_step_host_matches_device_path(d, orc, dtype, fg):
+    """gcn/gat_step_host (host buffers, overlapped copies) give exactly the
+    device-path results: same kernels, only the transfers differ."""
+    n, m, k, h, kk = 1800, 24, 40, 4, 8
+    _, s, t = orc.synthetic_graph(n, 9.0, 3)
+    src, dst = torch.from_numpy(s), torch.from_numpy(t)
+    A = d.Adjacency.gcn_operator(n, src, dst, dtype, "csc")
+    X = torch.rand(n, m, dtype=dtype) * 2 - 1
+    G = torch.rand(n, k, dtype=dtype) * 2 - 1
+    th, bi = d.gcn_params(m, k, 13, dtype=dtype)
+    for policy in ("adaptive", "transform-first", "propagate-first"):
+        sch = d.resolve_scheme(policy, m, k, bool(fg), True)
+        out, cache = d.gcn_forward(A, X.cuda(), th, bi, sch)
+        ref = (out,) + d.gcn_backward(A, G.cuda(), th, cache, bool(fg))
+        pin = lambda *sh: torch.empty(sh, dtype=dtype).pin_memory()  # noqa: E731
+        ho, hth, hb, hx = pin(n, k), pin(m, k), pin(k), pin(n, m)
+        d.gcn_step_host(A, X.pin_memory(), th, bi, sch, G.pin_memory(), bool(fg), ho, hth, hb,
+                        hx if fg else None)
+        A.ctx.synchronize()
+        got = (ho, hth, hb, hx if fg else None)
+        for a, b in zip(got, ref):
+            if b is None:
+                continue
+            assert torch.equal(a, b.cpu()), policy
+    P = d.Pattern.gat_pattern(n, src, dst)
+    th2, a_s, a_d, b2 = d.gat_params(m, h, kk, 23, dtype=dtype)
+    G2 = torch.rand(n, h * kk, dtype=dtype) * 2 - 1
+    for level in ("none", "full"):
+        o, c = d.gat_forward(P, X.cuda(), th2, a_s, a_d, b2, h, 0.2, level)
+        ref = (o,) + d.gat_backward(P, G2.cuda(), th2, a_s, a_d, c, bool(fg))
+        pin = lambda *sh: torch.empty(sh, dtype=dtype).pin_memory()  # noqa: E731
+        hs = (pin(n, h * kk), pin(m, h * kk), pin(h, kk), pin(h, kk), pin(h * kk), pin(n, m))
+        d.gat_step_host(P, X.pin_memory(), th2, a_s, a_d, b2, h, 0.2, level, G2.pin_memory(),
+                        bool(fg), *hs[:5], hs[5] if fg else None)
+        P.ctx.synchronize()
+        for a, b in zip(hs, ref):
+            if b is None:
+                continue
+            assert torch.equal(a, b.cpu()), level
