@@ -207,14 +207,74 @@ __global__ void __launch_bounds__(256) k_colsum_final(int32_t nchunks, int32_t c
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t j = blockIdx.x * 32 + lane;
   double s = 0.0;
-  if (j < cols)
-    for (int32_t c = w; c < nchunks; c += 8) s += part[(int64_t)c * cols + j];
+  if (j < cols) {  // four independent chains: the partial list is read latency-free
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int32_t c = w;
+    for (; c + 24 < nchunks; c += 32) {
+      s += part[(int64_t)c * cols + j];
+      s1 += part[(int64_t)(c + 8) * cols + j];
+      s2 += part[(int64_t)(c + 16) * cols + j];
+      s3 += part[(int64_t)(c + 24) * cols + j];
+    }
+    for (; c < nchunks; c += 8) s += part[(int64_t)c * cols + j];
+    s = (s + s1) + (s2 + s3);
+  }
   sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && j < cols) {
     double t = 0.0;
     for (int k = 0; k < 8; ++k) t += sh[k][lane];
     out[j] = (T)t;
+  }
+}
+
+// float rows of cols % 4 == 0 (cols <= 1024): threads own float4 column
+// vectors, 256 / (cols/4) row groups per block stride the chunk, float64
+// accumulation, row groups combined in a fixed order in shared memory.
+__global__ void __launch_bounds__(256) k_colsum_partial_v4(const float4* __restrict__ X,
+                                                           int32_t rows, int32_t nv,
+                                                           int32_t chunk,
+                                                           double* __restrict__ part) {
+  __shared__ double sh[256 * 4];
+  const int groups = max(1, 256 / nv);
+  const int tid = threadIdx.x, v = tid % nv, grp = tid / nv;
+  const int32_t r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (grp < groups) {
+    int32_t i = r0 + grp;
+    for (; i + groups < r1; i += 2 * groups) {
+      const float4 x = __ldg(X + (int64_t)i * nv + v);
+      const float4 y = __ldg(X + (int64_t)(i + groups) * nv + v);
+      a0 += (double)x.x + (double)y.x;
+      a1 += (double)x.y + (double)y.y;
+      a2 += (double)x.z + (double)y.z;
+      a3 += (double)x.w + (double)y.w;
+    }
+    if (i < r1) {
+      const float4 x = __ldg(X + (int64_t)i * nv + v);
+      a0 += x.x;
+      a1 += x.y;
+      a2 += x.z;
+      a3 += x.w;
+    }
+  }
+  sh[tid * 4] = a0;
+  sh[tid * 4 + 1] = a1;
+  sh[tid * 4 + 2] = a2;
+  sh[tid * 4 + 3] = a3;
+  __syncthreads();
+  if (grp == 0 && tid < nv) {
+    for (int g = 1; g < groups; ++g) {
+      a0 += sh[(g * nv + v) * 4];
+      a1 += sh[(g * nv + v) * 4 + 1];
+      a2 += sh[(g * nv + v) * 4 + 2];
+      a3 += sh[(g * nv + v) * 4 + 3];
+    }
+    double* o = part + (int64_t)blockIdx.x * nv * 4 + v * 4;
+    o[0] = a0;
+    o[1] = a1;
+    o[2] = a2;
+    o[3] = a3;
   }
 }
 
@@ -228,6 +288,11 @@ void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out) {
   DevBuf part((size_t)nchunks * cols * sizeof(double), ctx->stream);
   if (rows == 0) {
     SGNN_CUDA(cudaMemsetAsync(part.get(), 0, part.bytes(), ctx->stream));
+  } else if (sizeof(T) == 4 && cols % 4 == 0 && cols <= 1024 &&
+             reinterpret_cast<uintptr_t>(X) % 16 == 0) {
+    k_colsum_partial_v4<<<nchunks, 256, 0, ctx->stream>>>(
+        reinterpret_cast<const float4*>(X), rows, cols / 4, chunk, part.as<double>());
+    launched(ctx);
   } else {
     k_colsum_partial<T><<<nchunks, 256, 0, ctx->stream>>>(X, rows, cols, chunk,
                                                           part.as<double>());

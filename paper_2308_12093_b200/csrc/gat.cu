@@ -76,6 +76,7 @@ __device__ __forceinline__ void vstore(T* p, const T (&in)[W]) {
 }
 
 #include "gat_fast.cuh"
+#include "gat_v2.cuh"
 
 // kernels.hpp:385-423 node_scores: one thread per (node, head), sequential dot
 template <class T>
@@ -570,6 +571,35 @@ static int wgrid(int32_t n) {
     default: { constexpr int RR = 8; __VA_ARGS__; } break; \
   }
 
+// float32 compile-time-heads path (gat_v2.cuh): h in {1,2,4,8}, k/4 a power
+// of two <= 32.  Returns R (16-byte vectors per lane) or 0.
+template <class T>
+static int v2_R(int32_t h, int32_t k) {
+  if (sizeof(T) != 4 || getenv("SGNN_GAT_V1")) return 0;
+  if (!(h == 1 || h == 2 || h == 4 || h == 8) || k % 4 != 0) return 0;
+  const int L = k / 4;
+  if ((L & (L - 1)) != 0 || L > 32) return 0;
+  return pick_r(h * k / 4);
+}
+
+// (H, R) -> constexpr instantiation; R <= 32 * H / 32 lanes' worth
+#define HR_SWITCH(H_, R_, ...)                                                        \
+  switch (H_ * 16 + R_) {                                                             \
+    case 1 * 16 + 1: { constexpr int HH = 1, RR = 1; __VA_ARGS__; } break;          \
+    case 2 * 16 + 1: { constexpr int HH = 2, RR = 1; __VA_ARGS__; } break;          \
+    case 2 * 16 + 2: { constexpr int HH = 2, RR = 2; __VA_ARGS__; } break;          \
+    case 4 * 16 + 1: { constexpr int HH = 4, RR = 1; __VA_ARGS__; } break;          \
+    case 4 * 16 + 2: { constexpr int HH = 4, RR = 2; __VA_ARGS__; } break;          \
+    case 4 * 16 + 4: { constexpr int HH = 4, RR = 4; __VA_ARGS__; } break;          \
+    case 8 * 16 + 1: { constexpr int HH = 8, RR = 1; __VA_ARGS__; } break;          \
+    case 8 * 16 + 2: { constexpr int HH = 8, RR = 2; __VA_ARGS__; } break;          \
+    case 8 * 16 + 4: { constexpr int HH = 8, RR = 4; __VA_ARGS__; } break;          \
+    case 8 * 16 + 8: { constexpr int HH = 8, RR = 8; __VA_ARGS__; } break;          \
+    default: throw invalid_argument("gat: no v2 kernel for this head/width");        \
+  }
+
+static unsigned v2_grid(int32_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, g2::WPB)); }
+
 template <class T>
 static void node_scores_fast(sgnn_ctx ctx, int R, int32_t n, int32_t h, int32_t k, const T* M,
                              const T* a_src, const T* a_dst, T* s, T* d) {
@@ -594,7 +624,33 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
   const int32_t* rp = p->rowptr.as<int32_t>();
   const int32_t* ci = p->cols.as<int32_t>();
   const int R = fast_R<T>(h, k);
-  if (R && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
+  const int R2 = v2_R<T>(h, k);
+  if (R2 && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
+    node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+    const float4* M4 = reinterpret_cast<const float4*>(M.get());
+    const float4* b4 = reinterpret_cast<const float4*>(bias);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const float* sp = reinterpret_cast<const float*>(s.get());
+    const float* dp = reinterpret_cast<const float*>(d.get());
+    DevBuf alpha_tmp;
+    float* ap;
+    uint8_t* mp = nullptr;
+    if (level == SGNN_GAT_FULL) {
+      alpha = DevBuf((size_t)q * h * sizeof(T) + 16, st);
+      mask = DevBuf((size_t)q * h + 16, st);
+      ap = alpha.as<float>();
+      mp = mask.as<uint8_t>();
+    } else {
+      alpha_tmp = DevBuf((size_t)q * h * sizeof(T) + 16, st);
+      ap = alpha_tmp.as<float>();
+    }
+    HR_SWITCH(h, R2, (g2::k_gat_attn3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+                         n, rp, ci, sp, dp, (float)beta, ap, mp)));
+    launched(ctx);
+    HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, ap, M4, k,
+                                                                        b4, o4)));
+    launched(ctx);
+  } else if (R && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
     constexpr int VW = sizeof(T) == 4 ? 4 : 2;
     constexpr int wpb = gf::WPB<T>::v;
     node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
@@ -694,6 +750,54 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     mask_t = DevBuf((size_t)q * h + 8, st);
   }
   const T* alpha = cached ? c->alpha.as<T>() : alpha_t.as<T>();
+  const int R2 = v2_R<T>(h, k);
+  if (R2 && al16(G) && al16(r.Mp) && al16(dM.get()) && al16(a_src) && al16(a_dst)) {
+    const int32_t* rp = p->rowptr.as<int32_t>();
+    const int32_t* ci = p->cols.as<int32_t>();
+    const float4* M4 = reinterpret_cast<const float4*>(r.Mp);
+    const float4* G4 = reinterpret_cast<const float4*>(G);
+    const float* sp = reinterpret_cast<const float*>(r.sp);
+    const float* dp = reinterpret_cast<const float*>(r.dp);
+    if (!cached) {  // attention + mask recomputed like gat_recompute (gat.hpp:150-170)
+      HR_SWITCH(h, R2, (g2::k_gat_attn3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+                           n, rp, ci, sp, dp, (float)beta, alpha_t.as<float>(),
+                           mask_t.as<uint8_t>())));
+      launched(ctx);
+    }
+    const float* al = reinterpret_cast<const float*>(alpha);
+    const uint8_t* mk = cached ? c->mask.as<uint8_t>() : mask_t.as<uint8_t>();
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, M4, G4, k,
+                                                                          da.as<float>())));
+    launched(ctx);
+    HR_SWITCH(h, R2, (g2::k_gat_sbwd3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+                         n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
+                         dS.as<float>())));
+    launched(ctx);
+    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<v2_grid(n), 256, 0, st>>>(
+                         n, p->colptr.as<int32_t>(), p->rows.as<int32_t>(), p->perm.as<int32_t>(),
+                         G4, al, dy.as<float>(), dS.as<float>(),
+                         reinterpret_cast<const float4*>(a_src),
+                         reinterpret_cast<const float4*>(a_dst), k, dD.as<float>(),
+                         reinterpret_cast<float4*>(dM.get()))));
+    launched(ctx);
+    constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+    const int32_t chunk = (int32_t)std::max<int64_t>(64, ceil_div(n, ctx->num_sms * 4));
+    const int32_t nch = (int32_t)std::max<int64_t>(1, ceil_div(n, chunk));
+    DevBuf psrc((size_t)nch * hk * 8, st), pdst((size_t)nch * hk * 8, st);
+    gf::k_attgrad2_partial<T, VW><<<nch, 256, 0, st>>>(n, h, k, r.Mp, dS.as<T>(), dD.as<T>(),
+                                                      chunk, psrc.as<double>(), pdst.as<double>());
+    launched(ctx);
+    gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
+                                                                      psrc.as<double>(), d_a_src);
+    launched(ctx);
+    gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
+                                                                      pdst.as<double>(), d_a_dst);
+    launched(ctx);
+    gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
+            d_theta);
+    if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+    return;
+  }
   {
     const int R = fast_R<T>(h, k);
     if (R && al16(G) && al16(r.Mp) && al16(dM.get()) && al16(a_src) && al16(a_dst)) {

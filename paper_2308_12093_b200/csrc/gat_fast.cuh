@@ -703,8 +703,18 @@ __global__ void __launch_bounds__(256) k_reduce_partials(int32_t nw, int32_t hk,
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t c = blockIdx.x * 32 + lane;
   double s = 0.0;
-  if (c < hk)
-    for (int32_t z = w; z < nw; z += 8) s += part[(int64_t)z * hk + c];
+  if (c < hk) {  // four independent chains
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int32_t z = w;
+    for (; z + 24 < nw; z += 32) {
+      s += part[(int64_t)z * hk + c];
+      s1 += part[(int64_t)(z + 8) * hk + c];
+      s2 += part[(int64_t)(z + 16) * hk + c];
+      s3 += part[(int64_t)(z + 24) * hk + c];
+    }
+    for (; z < nw; z += 8) s += part[(int64_t)z * hk + c];
+    s = (s + s1) + (s2 + s3);
+  }
   sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < hk) {

@@ -1,0 +1,679 @@
+// gat_v2.cuh -- float32 GAT row/column kernels with compile-time head count
+// (included by gat.cu inside namespace sgnn).  Used when T = float, h is 1, 2,
+// 4 or 8, k % 4 == 0 and k/4 is a power of two <= 32 (a head spans k/4 lanes
+// of one 32-lane chunk); other shapes use gat_fast.cuh / the generic kernels.
+//
+// Against gat_fast.cuh (which folds the softmax statistics by lanes over heads
+// in stored edge order, one dependent shared-memory round trip per edge) these
+// kernels keep every per-edge scalar in registers of the lane that owns the
+// edge and reduce over the warp with a transposed butterfly: h values per lane
+// are reduced across 32 lanes in (h-1) + (5-log2 h) shuffles, then broadcast
+// back in h shuffles -- 17 shuffles for 8 heads instead of 40.  The float32
+// path is checked against the float64 oracle at the north-star tolerance
+// (1e-4 under max_rel_diff, dense.hpp:303-316); softmax sums therefore use a
+// tree order and products use FMA, where gat_fast.cuh reproduces the
+// reference's sequential order.  Dense-row gathers are issued U = 4 edges
+// ahead (R 16-byte vectors per lane per edge) to keep more bytes in flight.
+//
+// Reference semantics followed: kernels.hpp:427-534 (scores, LeakyReLU, edge
+// softmax, alpha = exp(w - max) * (1 / sum)), 219-254 (semibatched SpMM),
+// 342-377 (SDDMM dAlpha), 481-495 + 537-588 (softmax / LeakyReLU backward,
+// row sums), 258-295 + 614-658 (transposed semibatched SpMM, column sums,
+// add_scaled_rows).
+#pragma once
+
+namespace g2 {
+
+constexpr int WPB = 8;  // warps (rows) per block
+
+// dense-row gathers in flight per warp: 4 16-byte vectors per lane in total
+template <int R>
+struct Unroll {
+  static constexpr int v = R >= 4 ? 1 : 4 / R;
+};
+
+template <int H>
+struct Log2 {
+  static constexpr int v = H == 1 ? 0 : H == 2 ? 1 : H == 4 ? 2 : H == 8 ? 3 : 4;
+};
+
+struct OpMax {
+  __device__ __forceinline__ float operator()(float a, float b) const { return fmaxf(a, b); }
+};
+struct OpSum {
+  __device__ __forceinline__ float operator()(float a, float b) const { return a + b; }
+};
+
+// Reduce v[0..H) over all 32 lanes; on return every lane holds all H results.
+template <int H, class Op>
+__device__ __forceinline__ void allreduce(float (&v)[H], int lane, Op op) {
+  constexpr int LG = Log2<H>::v;
+#pragma unroll
+  for (int s = 0; s < LG; ++s) {  // reduce-scatter: halve the live values each step
+    const int o = 16 >> s;
+    const int half = H >> (s + 1);
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      const float send = up ? v[q] : v[q + half];
+      const float keep = up ? v[q + half] : v[q];
+      v[q] = op(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> LG; o > 0; o >>= 1) v[0] = op(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+  // lane l now holds head ((l >> (5 - LG)) bit-reversed order below) -- gather back
+  const float mine = v[0];
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    // head t was kept by lanes whose bits (4, 3, ...) spell t from the top half down
+    int src = 0;
+#pragma unroll
+    for (int s = 0; s < LG; ++s)
+      if (t & (H >> (s + 1))) src |= 16 >> s;
+    v[t] = __shfl_sync(0xffffffffu, mine, src);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void ld_heads(const float* __restrict__ p, float (&v)[H]) {
+  if constexpr (H % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < H / 4; ++q) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p) + q);
+      v[4 * q] = x.x;
+      v[4 * q + 1] = x.y;
+      v[4 * q + 2] = x.z;
+      v[4 * q + 3] = x.w;
+    }
+  } else if constexpr (H == 2) {
+    const float2 x = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = x.x;
+    v[1] = x.y;
+  } else {
+    v[0] = __ldg(p);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void st_heads(float* __restrict__ p, const float (&v)[H]) {
+  if constexpr (H % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < H / 4; ++q)
+      reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else if constexpr (H == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+    p[0] = v[0];
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void st_mask(uint8_t* __restrict__ p, uint32_t bits) {
+  if constexpr (H == 8) {
+    uint2 w;
+    w.x = (bits & 1u) | ((bits >> 1) & 1u) << 8 | ((bits >> 2) & 1u) << 16 | ((bits >> 3) & 1u) << 24;
+    w.y = ((bits >> 4) & 1u) | ((bits >> 5) & 1u) << 8 | ((bits >> 6) & 1u) << 16 |
+          ((bits >> 7) & 1u) << 24;
+    *reinterpret_cast<uint2*>(p) = w;
+  } else if constexpr (H == 4) {
+    *reinterpret_cast<uint32_t*>(p) =
+        (bits & 1u) | ((bits >> 1) & 1u) << 8 | ((bits >> 2) & 1u) << 16 | ((bits >> 3) & 1u) << 24;
+  } else if constexpr (H == 2) {
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)((bits & 1u) | ((bits >> 1) & 1u) << 8);
+  } else {
+    p[0] = (uint8_t)(bits & 1u);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ uint32_t ld_mask(const uint8_t* __restrict__ p) {
+  uint32_t w0 = 0, w1 = 0;
+  if constexpr (H == 8) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+    w0 = w.x;
+    w1 = w.y;
+  } else if constexpr (H == 4) {
+    w0 = __ldg(reinterpret_cast<const uint32_t*>(p));
+  } else if constexpr (H == 2) {
+    w0 = __ldg(reinterpret_cast<const uint16_t*>(p));
+  } else {
+    w0 = __ldg(p);
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    const uint32_t b = t < 4 ? (w0 >> (8 * t)) & 0xffu : (w1 >> (8 * (t - 4))) & 0xffu;
+    bits |= (b != 0u ? 1u : 0u) << t;
+  }
+  return bits;
+}
+
+__device__ __forceinline__ float lrelu(float y, float beta) { return y > 0.f ? y : beta * y; }
+
+__device__ __forceinline__ void fma4(float4& a, float s, const float4& b) {
+  a.x = fmaf(s, b.x, a.x);
+  a.y = fmaf(s, b.y, a.y);
+  a.z = fmaf(s, b.z, a.z);
+  a.w = fmaf(s, b.w, a.w);
+}
+__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
+  return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
+}
+
+// Per-row softmax statistics over [beg, end): mx[t] = max_e w, inv[t] =
+// 1 / sum_e exp(w - mx).  Rows of <= 32 edges keep the lane's scores in
+// e[] (= exp(w - mx)) for the caller; longer rows recompute.
+template <int H>
+__device__ __forceinline__ void row_stats(int lane, int32_t beg, int32_t end,
+                                          const int32_t* __restrict__ cols,
+                                          const float* __restrict__ d, const float (&si)[H],
+                                          float beta, float (&mx)[H], float (&inv)[H],
+                                          float (&e)[H], uint32_t& pos) {
+  float w[H];
+  pos = 0;
+#pragma unroll
+  for (int t = 0; t < H; ++t) mx[t] = -INFINITY;
+  for (int32_t base = beg; base < end; base += 32) {
+    const int32_t ee = base + lane;
+    if (ee < end) {
+      float dj[H];
+      ld_heads<H>(d + (int64_t)__ldg(cols + ee) * H, dj);
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        const float y = si[t] + dj[t];
+        w[t] = lrelu(y, beta);
+        if (base == beg && y > 0.f) pos |= 1u << t;
+        mx[t] = fmaxf(mx[t], w[t]);
+      }
+    }
+  }
+  allreduce<H>(mx, lane, OpMax());
+  float sm[H];
+  const bool single = end - beg <= 32;
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    e[t] = (single && beg + lane < end) ? __expf(w[t] - mx[t]) : 0.f;
+    sm[t] = e[t];
+  }
+  if (!single) {
+    for (int32_t base = beg; base < end; base += 32) {
+      const int32_t ee = base + lane;
+      if (ee < end) {
+        float dj[H];
+        ld_heads<H>(d + (int64_t)__ldg(cols + ee) * H, dj);
+#pragma unroll
+        for (int t = 0; t < H; ++t) sm[t] += __expf(lrelu(si[t] + dj[t], beta) - mx[t]);
+      }
+    }
+  }
+  allreduce<H>(sm, lane, OpSum());
+#pragma unroll
+  for (int t = 0; t < H; ++t) inv[t] = 1.f / sm[t];
+}
+
+// alpha of the lane's edge ee for every head (multi-batch rows: recomputed)
+template <int H>
+__device__ __forceinline__ void edge_alpha(int32_t ee, const int32_t* __restrict__ cols,
+                                           const float* __restrict__ d, const float (&si)[H],
+                                           float beta, const float (&mx)[H], const float (&inv)[H],
+                                           float (&a)[H], uint32_t& pos) {
+  float dj[H];
+  ld_heads<H>(d + (int64_t)__ldg(cols + ee) * H, dj);
+  pos = 0;
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    const float y = si[t] + dj[t];
+    if (y > 0.f) pos |= 1u << t;
+    a[t] = __expf(lrelu(y, beta) - mx[t]) * inv[t];
+  }
+}
+
+// Aggregate one staged batch: acc[r] += sum_j alpha[j][head(r)] * X[col_j] (R
+// 16-byte vectors per lane), U gathers in flight.
+template <int H, int R>
+__device__ __forceinline__ void aggregate(int lane, int cnt, int32_t mycol, int fv,
+                                          const float4* __restrict__ X,
+                                          float (*sa)[H + 1], const int (&tr)[R],
+                                          float4 (&acc)[R]) {
+  constexpr int U = Unroll<R>::v;
+  for (int jb = 0; jb < cnt; jb += U) {
+    float4 x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + u;
+      const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, mycol, j < cnt ? j : jb);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t v = r * 32 + lane;
+        if (j < cnt && v < (uint32_t)fv) x[u][r] = __ldg(X + c * (uint32_t)fv + v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (jb + u < cnt) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r * 32 + lane < fv) fma4(acc[r], sa[jb + u][tr[r]], x[u][r]);
+      }
+    }
+  }
+}
+
+// Softmax statistics of a row, staged for the warp: single-batch rows (<= 32
+// edges) leave alpha of every (edge, head) in sa[lane][t]; longer rows leave
+// (s_i, max, 1/sum) in st[0..2][t] for per-batch recomputation.  pos = the
+// lane's LeakyReLU mask bits (single-batch rows).
+template <int H>
+__device__ __forceinline__ uint32_t stage_stats(int lane, int32_t i, int32_t beg, int32_t end,
+                                                const int32_t* __restrict__ cols,
+                                                const float* __restrict__ s,
+                                                const float* __restrict__ d, float beta,
+                                                float (*sa)[H + 1], float (*st)[H]) {
+  float si[H], mx[H], inv[H], e[H];
+  uint32_t pos = 0;
+  ld_heads<H>(s + (int64_t)i * H, si);
+  row_stats<H>(lane, beg, end, cols, d, si, beta, mx, inv, e, pos);
+  if (end - beg <= 32) {
+    if (beg + lane < end)
+#pragma unroll
+      for (int t = 0; t < H; ++t) sa[lane][t] = e[t] * inv[t];
+  } else if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      st[0][t] = si[t];
+      st[1][t] = mx[t];
+      st[2][t] = inv[t];
+    }
+  }
+  __syncwarp();
+  return pos;
+}
+
+// alpha of edge ee of a multi-batch row from the staged statistics
+template <int H>
+__device__ __forceinline__ uint32_t restage_alpha(int32_t ee, const int32_t* __restrict__ cols,
+                                                  const float* __restrict__ d, float beta,
+                                                  const float (*st)[H], float* a) {
+  float dj[H];
+  ld_heads<H>(d + (int64_t)__ldg(cols + ee) * H, dj);
+  uint32_t pos = 0;
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    const float y = st[0][t] + dj[t];
+    if (y > 0.f) pos |= 1u << t;
+    a[t] = __expf(lrelu(y, beta) - st[1][t]) * st[2][t];
+  }
+  return pos;
+}
+
+// ---------------------------------------------------------------------------
+// forward, part 1 (kernels.hpp:427-534): attention of every (edge, head),
+// written edge-major (q x h) with the LeakyReLU mask.  A warp owns 32 rows;
+// each thread walks its own row (<= TMAX edges) serially: one online pass for
+// (max, sum) -- the running sum is rescaled when the max grows -- and one pass
+// writing alpha = exp(w - max) * (1 / sum).  The neighbour's score row (h
+// floats) is one 32-byte gather per edge; the second pass hits L1.  Rows
+// longer than TMAX are then done by the whole warp, lanes over edges.
+// ---------------------------------------------------------------------------
+constexpr int TMAX = 32;
+
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_attn3(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const int32_t* __restrict__ cols,
+                                                   const float* __restrict__ s,
+                                                   const float* __restrict__ d, float beta,
+                                                   float* __restrict__ alpha,
+                                                   uint8_t* __restrict__ mask) {
+  __shared__ float sh_a[WPB][32][H + 1];
+  __shared__ float sh_st[WPB][3][H];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t i = ((int32_t)blockIdx.x * WPB + wib) * 32 + lane;
+  int32_t beg = 0, end = 0;
+  if (i < n) {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+  }
+  const bool longrow = end - beg > TMAX;
+  if (i < n && !longrow) {
+    float si[H], mx[H], sm[H];
+    ld_heads<H>(s + (int64_t)i * H, si);
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      mx[t] = -INFINITY;
+      sm[t] = 0.f;
+    }
+    for (int32_t e = beg; e < end; ++e) {
+      float dj[H];
+      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        const float w = lrelu(si[t] + dj[t], beta);
+        const float mn = fmaxf(mx[t], w);
+        sm[t] = sm[t] * __expf(mx[t] - mn) + __expf(w - mn);
+        mx[t] = mn;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
+    for (int32_t e = beg; e < end; ++e) {
+      float dj[H], a[H];
+      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+      uint32_t pos = 0;
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        const float y = si[t] + dj[t];
+        if (y > 0.f) pos |= 1u << t;
+        a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+      }
+      st_heads<H>(alpha + (int64_t)e * H, a);
+      if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
+    }
+  }
+  uint32_t lm = __ballot_sync(0xffffffffu, i < n && longrow);
+  float(*sa)[H + 1] = sh_a[wib];
+  float(*st)[H] = sh_st[wib];
+  while (lm) {
+    const int src = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int32_t row = __shfl_sync(0xffffffffu, i, src);
+    const int32_t rb = __shfl_sync(0xffffffffu, beg, src);
+    const int32_t re = __shfl_sync(0xffffffffu, end, src);
+    stage_stats<H>(lane, row, rb, re, cols, s, d, beta, sa, st);  // > 32 edges: stats in st
+    for (int32_t ee = rb + lane; ee < re; ee += 32) {
+      float a[H];
+      const uint32_t pos = restage_alpha<H>(ee, cols, d, beta, st, a);
+      st_heads<H>(alpha + (int64_t)ee * H, a);
+      if (mask) st_mask<H>(mask + (int64_t)ee * H, pos);
+    }
+    __syncwarp();
+  }
+}
+
+static inline unsigned attn3_grid(int32_t n) {
+  return (unsigned)((n + 32 * WPB - 1) / (32 * WPB));
+}
+
+// ---------------------------------------------------------------------------
+// forward, part 2 (kernels.hpp:219-254 semibatched SpMM + bias):
+// out[i, t, :] = sum_e alpha[e, t] M[col_e, t, :] + b.  Lean like the GCN
+// SpMM: one warp per row, per edge a broadcast column index, one 4-byte
+// attention load per lane (its head; 32-byte sector per edge) and R 16-byte
+// row vectors, U edges in flight; <= 40 registers for 48 resident warps/SM.
+// ---------------------------------------------------------------------------
+template <int H, int R>
+__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
+    k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+               const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
+               const float4* __restrict__ bias, float4* __restrict__ out) {
+  constexpr int U = R >= 4 ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (i >= n) return;
+  const int fv = H * k / 4, L = k / 4;
+  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  int tr[R];
+  float4 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    tr[r] = min(H - 1, (r * 32 + lane) / L);
+    acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  int32_t e = beg;
+  for (; e + U <= end; e += U) {
+    uint32_t c[U];
+    float a[U][R];
+    float4 x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = (uint32_t)__ldg(cols + e + u);
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[u][r] = __ldg(alpha + (int64_t)(e + u) * H + tr[r]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t v = r * 32 + lane;
+        if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
+  }
+  for (; e < end; ++e) {
+    const uint32_t c = (uint32_t)__ldg(cols + e);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t v = r * 32 + lane;
+      if (v < (uint32_t)fv)
+        fma4(acc[r], __ldg(alpha + (int64_t)e * H + tr[r]), __ldg(M + c * (uint32_t)fv + v));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int v = r * 32 + lane;
+    if (v < fv) {
+      const float4 b = __ldg(bias + v);
+      float4 o = acc[r];
+      o.x += b.x;
+      o.y += b.y;
+      o.z += b.z;
+      o.w += b.w;
+      __stcs(out + (int64_t)i * fv + v, o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, part 1 (kernels.hpp:342-377 semibatched SDDMM): dAlpha[e, t] =
+// <dX'[i, t, :], M[col_e, t, :]>, edge-major.  Lean warp per row: the row of
+// dX' stays in registers, R 16-byte vectors of M gathered per edge, U edges
+// in flight, head-segmented xor reductions over the k/4 lanes of a head.
+// ---------------------------------------------------------------------------
+template <int H, int R>
+__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
+    k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                 const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
+                 float* __restrict__ da) {
+  constexpr int U = R >= 4 ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (i >= n) return;
+  const int fv = H * k / 4, L = k / 4;
+  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  int tr[R];
+  float4 g[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int v = r * 32 + lane;
+    tr[r] = min(H - 1, v / L);
+    g[r] = v < fv ? __ldg(G + (int64_t)i * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const bool lead = (lane & (L - 1)) == 0;
+  for (int32_t e = beg; e < end; e += U) {
+    uint32_t c[U];
+    float4 x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (uint32_t)__ldg(cols + min(e + u, end - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t v = r * 32 + lane;
+        if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float p[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) p[r] = r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
+      for (int o = L >> 1; o > 0; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
+      if (lead && e + u < end)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r * 32 + lane < fv) da[(int64_t)(e + u) * H + tr[r]] = p[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, part 2 (kernels.hpp:537-567 softmax backward, 481-495 LeakyReLU
+// backward, 571-588 row sums): per row, dot[t] = sum_e alpha dAlpha, dy =
+// mask ? dw : beta dw with dw = alpha (dAlpha - dot), dS[i, t] = sum_e dy.
+// Thread per row (<= TMAX edges), the whole warp for longer rows.
+// ---------------------------------------------------------------------------
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_sbwd3(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const float* __restrict__ alpha,
+                                                   const uint8_t* __restrict__ mask,
+                                                   const float* __restrict__ da, float beta,
+                                                   float* __restrict__ dy,
+                                                   float* __restrict__ dS) {
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t i = ((int32_t)blockIdx.x * WPB + wib) * 32 + lane;
+  int32_t beg = 0, end = 0;
+  if (i < n) {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+  }
+  const bool longrow = end - beg > TMAX;
+  auto finish = [&](int32_t e, const float (&dot)[H], float (&rs)[H]) {
+    float a[H], g[H], y[H];
+    ld_heads<H>(alpha + (int64_t)e * H, a);
+    ld_heads<H>(da + (int64_t)e * H, g);
+    const uint32_t pos = ld_mask<H>(mask + (int64_t)e * H);
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      const float dw = a[t] * (g[t] - dot[t]);
+      y[t] = (pos >> t) & 1u ? dw : beta * dw;
+      rs[t] += y[t];
+    }
+    st_heads<H>(dy + (int64_t)e * H, y);
+  };
+  if (i < n && !longrow) {
+    float dot[H], rs[H];
+#pragma unroll
+    for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
+    for (int32_t e = beg; e < end; ++e) {
+      float a[H], g[H];
+      ld_heads<H>(alpha + (int64_t)e * H, a);
+      ld_heads<H>(da + (int64_t)e * H, g);
+#pragma unroll
+      for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
+    }
+    for (int32_t e = beg; e < end; ++e) finish(e, dot, rs);
+    st_heads<H>(dS + (int64_t)i * H, rs);
+  }
+  uint32_t lm = __ballot_sync(0xffffffffu, i < n && longrow);
+  while (lm) {
+    const int src = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int32_t row = __shfl_sync(0xffffffffu, i, src);
+    const int32_t rb = __shfl_sync(0xffffffffu, beg, src);
+    const int32_t re = __shfl_sync(0xffffffffu, end, src);
+    float dot[H], rs[H];
+#pragma unroll
+    for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
+    for (int32_t e = rb + lane; e < re; e += 32) {
+      float a[H], g[H];
+      ld_heads<H>(alpha + (int64_t)e * H, a);
+      ld_heads<H>(da + (int64_t)e * H, g);
+#pragma unroll
+      for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
+    }
+    allreduce<H>(dot, lane, OpSum());
+    for (int32_t e = rb + lane; e < re; e += 32) finish(e, dot, rs);
+    allreduce<H>(rs, lane, OpSum());
+    if (lane == 0) st_heads<H>(dS + (int64_t)row * H, rs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, part 3, per source column j over the CSC view (kernels.hpp:
+// 258-295 transposed semibatched SpMM, 640-658 column sums, 614-636
+// add_scaled_rows): dM[j] = sum_e alpha[e] dX'[row_e] + dS[j] a_src + dD[j]
+// a_dst with dD[j, t] = sum_e dy[e, t].  Lean warp per column: per edge the
+// canonical index and row are broadcast loads, alpha / dy one 4-byte load per
+// lane (its head), the dX' row R 16-byte vectors; the lanes of a head carry
+// identical dD sums, so no reduction is needed.
+// ---------------------------------------------------------------------------
+template <int H, int R>
+__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
+    int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
+    const int32_t* __restrict__ perm, const float4* __restrict__ G,
+    const float* __restrict__ alpha, const float* __restrict__ dy, const float* __restrict__ dS,
+    const float4* __restrict__ a_src, const float4* __restrict__ a_dst, int32_t k,
+    float* __restrict__ dD, float4* __restrict__ dM) {
+  constexpr int U = R >= 4 ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (j >= n) return;
+  const int fv = H * k / 4, L = k / 4;
+  const int32_t beg = __ldg(colptr + j), end = __ldg(colptr + j + 1);
+  int tr[R];
+  float4 acc[R];
+  float dd[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    tr[r] = min(H - 1, (r * 32 + lane) / L);
+    acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dd[r] = 0.f;
+  }
+  int32_t p = beg;
+  for (; p + U <= end; p += U) {
+    uint32_t row[U];
+    int32_t e[U];
+    float a[U][R];
+    float4 x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      e[u] = __ldg(perm + p + u);
+      row[u] = (uint32_t)__ldg(crows + p + u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t v = r * 32 + lane;
+        a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
+        dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
+        if (v < (uint32_t)fv) x[u][r] = __ldg(G + row[u] * (uint32_t)fv + v);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
+  }
+  for (; p < end; ++p) {
+    const int32_t e = __ldg(perm + p);
+    const uint32_t row = (uint32_t)__ldg(crows + p);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t v = r * 32 + lane;
+      const float a = __ldg(alpha + (int64_t)e * H + tr[r]);
+      dd[r] += __ldg(dy + (int64_t)e * H + tr[r]);
+      if (v < (uint32_t)fv) fma4(acc[r], a, __ldg(G + row * (uint32_t)fv + v));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int v = r * 32 + lane;
+    if (v < fv) {
+      if ((lane & (L - 1)) == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
+      const float cs = __ldg(dS + (int64_t)j * H + tr[r]);
+      const float4 as = __ldg(a_src + v), ad = __ldg(a_dst + v);
+      float4 o = acc[r];
+      fma4(o, cs, as);
+      fma4(o, dd[r], ad);
+      __stcs(dM + (int64_t)j * fv + v, o);
+    }
+  }
+}
+
+}  // namespace g2
