@@ -240,6 +240,41 @@ int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache cach
                                const void* theta, const void* a_src, const void* a_dst,
                                void* alpha_hq, uint8_t* mask_hq);
 
+/* ---- two-layer models (model.hpp:16-245) ---------------------------------
+ * Gcn2 = GCN -> ReLU -> GCN, Gat2 = GAT -> ELU(1) -> GAT; replaces Gcn2Model /
+ * Gat2Model + loss_mse (model.hpp) and activation / activation_backward
+ * (dense.hpp:190-270).  Parameters are device buffers owned by the model,
+ * initialised like the constructors (layer 2 from seed+101 / seed+201). */
+typedef struct {
+  int32_t kind;          /* ModelKind: 0 gcn2, 1 gat2 (model.hpp:16) */
+  int32_t in_features;   /* ModelConfig (model.hpp:18-29) */
+  int32_t hidden;
+  int32_t out_features;
+  int32_t heads;         /* gat2 */
+  int32_t scheme_policy; /* SchemePolicy: 0 adaptive, 1 transform-first, 2 propagate-first */
+  int32_t caching;       /* gcn2: retain A'X */
+  int32_t gat_level;     /* gat2: sgnn_gat_level */
+  double leaky_slope;    /* gat attention slope */
+  int32_t input_grad;    /* compute d(input features) */
+} sgnn_model_config;
+typedef struct sgnn_model_s* sgnn_model;
+int sgnn_model_create(sgnn_ctx ctx, const sgnn_model_config* cfg, uint64_t seed, int dtype,
+                      sgnn_model* out);
+int sgnn_model_destroy(sgnn_model model);
+/* param_tensors() (model.hpp:100-107, 208-218): count, then (device data,
+ * element count, name) of tensor i */
+int sgnn_model_num_params(sgnn_model model, int32_t* count);
+int sgnn_model_param(sgnn_model model, int32_t i, void** data, int64_t* size, const char** name);
+/* One training step (bench.hpp:193-219): forward, loss_mse(out, target),
+ * backward.  adj for gcn2, pattern for gat2; out (optional) receives the
+ * prediction; grads[i] receives the gradient of parameter i (device buffers,
+ * param_tensors() order); d_input is required when cfg.input_grad; loss
+ * (optional) is a DEVICE double receiving the mean squared error.
+ * Stream-ordered, no host synchronisation. */
+int sgnn_model_train_step(sgnn_ctx ctx, sgnn_model model, sgnn_adj adj, sgnn_pattern pattern,
+                          const void* X, const void* target, void* out, void* const* grads,
+                          void* d_input, double* loss);
+
 /* ---- host-buffer layer steps (pipeline.cu) -------------------------------
  * One forward + backward step with HOST inputs and outputs, the shape of the
  * reference API (DenseMatrix in host memory, gcn.hpp:91-193 / gat.hpp:89-219)

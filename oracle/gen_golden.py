@@ -254,5 +254,39 @@ def main():
     save("gat", **gat)
 
 
+# two-layer models (model.hpp): (kind, n, deg, seed, m, hidden, out, heads,
+# policy, caching, level, input_grad)
+MODEL_CASES = {
+    "gcn2_adaptive_cached": (0, 300, 6.0, 5, 12, 16, 5, 1, 0, 1, 0, 0),
+    "gcn2_adaptive_fg": (0, 300, 6.0, 5, 12, 16, 5, 1, 0, 0, 0, 1),
+    "gcn2_tf": (0, 250, 4.0, 9, 20, 8, 3, 1, 1, 0, 0, 1),
+    "gat2_h2": (1, 200, 5.0, 7, 10, 4, 3, 2, 0, 0, 3, 1),
+    "gat2_h8": (1, 220, 6.0, 3, 16, 8, 4, 8, 0, 0, 3, 0),
+}
+
+
+def models():
+    out = {}
+    for tag, (kind, n, deg, seed, m, hid, o, h, pol, ca, lv, ig) in MODEL_CASES.items():
+        ow = o if kind == 0 else h * o
+        sizes = ([m * hid, hid, hid * o, o] if kind == 0 else
+                 [m * h * hid, h * hid, h * hid, h * hid, h * hid * h * o, h * o, h * o, h * o])
+        loss = C.c_double()
+        pred = np.empty((n, ow))
+        grads = np.empty(sum(sizes))
+        assert L.ref_model_step(kind, n, deg, seed, m, hid, o, h, pol, ca, lv, ig,
+                                C.byref(loss), pred, grads) == 0, L.ref_last_error()
+        out[f"{tag}_loss"] = np.array([loss.value])
+        out[f"{tag}_pred"] = pred
+        out[f"{tag}_grads"] = grads
+        out[f"{tag}_cfg"] = np.array([kind, n, seed, m, hid, o, h, pol, ca, lv, ig], np.int64)
+        out[f"{tag}_deg"] = np.array([deg])
+    save("models", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["models"]:
+        models()
+    else:
+        main()
+        models()

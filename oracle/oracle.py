@@ -421,3 +421,46 @@ def gat_backward(pat: Operator, G, X, theta, a_src, a_dst, heads, beta=0.2, fg=F
                           theta, _f64(a_src), _f64(a_dst), heads, k, beta, int(fg), dth, das,
                           dad, db, _ptr(dx))
     return dth, das, dad, db, dx
+
+
+# ---- two-layer models (model.hpp:40-245) -----------------------------------
+def gcn2_params(m, hidden, out, seed):
+    """Gcn2Model(cfg, seed): layer 2 from seed+101 (model.hpp:46-49)."""
+    return gcn_params(m, hidden, seed) + gcn_params(hidden, out, seed + 101)
+
+
+def gat2_params(m, heads, hidden, out, seed):
+    """Gat2Model(cfg, seed): layer 2 input heads*hidden, seed+201 (model.hpp:126-130)."""
+    return gat_params(m, heads, hidden, seed) + gat_params(heads * hidden, heads, out, seed + 201)
+
+
+def gcn2_step(op: Operator, X, params, target, policy=0, caching=False, input_grad=False):
+    """Gcn2Model forward (model.hpp:52-69), loss_mse, backward (model.hpp:71-81).
+    Returns (loss, out, [dth1, db1, dth2, db2], dX-or-None)."""
+    th1, b1, th2, b2 = params
+    m, hid = th1.shape
+    k = th2.shape[1]
+    s1 = resolve_scheme(policy, m, hid, input_grad, caching)
+    s2 = resolve_scheme(policy, hid, k, True, caching)  # model.hpp:61-62
+    o1, P1 = gcn_forward(op, X, th1, b1, s1[0])
+    h, mask = activation(o1, "relu")
+    out, P2 = gcn_forward(op, h, th2, b2, s2[0])
+    loss, g = loss_mse(out, target)
+    dth2, db2, dh = gcn_backward(op, g, P2 if s2[1] == 2 else h, th2, s2[1], True)
+    dh = activation_backward(dh, mask, "relu")
+    dth1, db1, dx = gcn_backward(op, dh, P1 if s1[1] == 2 else X, th1, s1[1], input_grad)
+    return loss, out, [dth1, db1, dth2, db2], dx
+
+
+def gat2_step(pat: Operator, X, params, heads, target, beta=0.2, input_grad=False):
+    """Gat2Model forward (model.hpp:133-150), loss_mse, backward (model.hpp:152-163);
+    the cache level does not change the values (gat.hpp:150-170)."""
+    th1, as1, ad1, b1, th2, as2, ad2, b2 = params
+    o1 = gat_forward(pat, X, th1, as1, ad1, b1, heads, beta)
+    h, mask = activation(o1, "elu", 1.0)
+    out = gat_forward(pat, h, th2, as2, ad2, b2, heads, beta)
+    loss, g = loss_mse(out, target)
+    g2 = gat_backward(pat, g, h, th2, as2, ad2, heads, beta, True)
+    dh = activation_backward(g2[4], mask, "elu", 1.0, h)
+    g1 = gat_backward(pat, dh, X, th1, as1, ad1, heads, beta, input_grad)
+    return loss, out, list(g1[:4]) + list(g2[:4]), g1[4]

@@ -316,6 +316,63 @@ int ref_gat_layer(int n, const int* rowptr, const int* cols, const double* X, in
   }
 }
 
+// One training step of Gcn2Model (kind 0) / Gat2Model (kind 1) in double on
+// the workload of run_benchmark_typed (bench.hpp:160-219): graph from
+// synthetic_graph(n, deg, seed), X seed+11, target seed+12, model seed+13.
+// Writes the loss, the prediction and the gradients flattened in
+// param_tensors() order (grad_vectors, model.hpp:109-115 / 220-228).
+int ref_model_step(int kind, int n, double deg, unsigned long long seed, int m, int hidden,
+                   int out_f, int heads, int policy, int caching, int level, int input_grad,
+                   double* loss, double* pred, double* grads) {
+  try {
+    Graph g = synthetic_graph(n, deg, seed);
+    ModelConfig mc;
+    mc.kind = kind == 0 ? ModelKind::gcn2 : ModelKind::gat2;
+    mc.in_features = m;
+    mc.hidden = hidden;
+    mc.out_features = out_f;
+    mc.heads = heads;
+    mc.scheme = static_cast<SchemePolicy>(policy);
+    mc.caching = caching != 0;
+    mc.gat_level = static_cast<GatCacheLevel>(level);
+    mc.input_grad = input_grad != 0;
+    auto X = DenseMatrix<double>::random_uniform(n, m, seed + 11);
+    const index_t ow = kind == 0 ? out_f : heads * out_f;
+    auto target = DenseMatrix<double>::random_uniform(n, ow, seed + 12);
+    std::vector<std::vector<double>> gv;
+    if (kind == 0) {
+      Gcn2Model<double> model(mc, seed + 13);
+      AdjacencyOp<double> adj(
+          convert(gcn_normalize(SparseMatrix<double>{adjacency<double>(g)}), SparseFormat::csc));
+      typename Gcn2Model<double>::Caches caches;
+      auto o = model.forward(X, adj, caches);
+      auto l = loss_mse(o, target);
+      *loss = l.value;
+      out(o, pred);
+      gv = Gcn2Model<double>::grad_vectors(model.backward(l.grad, adj, caches));
+    } else {
+      Gat2Model<double> model(mc, seed + 13);
+      auto csr = coo_to_csr(to_coo(add_self_loops(SparseMatrix<double>{adjacency<double>(g)})));
+      auto pattern = SparsePattern::from_csr(csr);
+      typename Gat2Model<double>::Caches caches;
+      auto o = model.forward(X, pattern, caches);
+      auto l = loss_mse(o, target);
+      *loss = l.value;
+      out(o, pred);
+      gv = Gat2Model<double>::grad_vectors(model.backward(l.grad, pattern, caches));
+    }
+    std::size_t off = 0;
+    for (const auto& v : gv) {
+      std::memcpy(grads + off, v.data(), sizeof(double) * v.size());
+      off += v.size();
+    }
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // CPU timing harness for bench.py (reference arm and cpu_baseline): builds the
 // workload exactly like run_benchmark_typed (bench.hpp:160-219) -- X from

@@ -55,6 +55,8 @@ def load():
                                 INT, INT, INT, VP, INT, f64p, VP, VP, VP]),
         "ref_gat_layer": (INT, [INT, i32p, i32p, f64p, INT, f64p, f64p, f64p, f64p, INT, INT,
                                 D, INT, VP, INT, f64p, VP, VP, VP, VP, VP, VP, VP]),
+        "ref_model_step": (INT, [INT, INT, D, ULL, INT, INT, INT, INT, INT, INT, INT, INT,
+                                 C.POINTER(D), f64p, f64p]),
         "ref_bench_create": (VP, [INT, INT, D, ULL, INT, INT, INT, INT, INT, INT, INT, INT]),
         "ref_bench_nnz": (LL, [VP]),
         "ref_bench_step": (D, [VP]),

@@ -30,6 +30,14 @@ POLICIES = {"adaptive": 0, "transform-first": 1, "propagate-first": 2}
 LEVELS = {"none": 0, "features": 1, "node-attn": 2, "full": 3}
 
 
+class ModelConfig(C.Structure):
+    """sgnn_model_config (model.hpp:18-29 ModelConfig)."""
+    _fields_ = [("kind", C.c_int32), ("in_features", C.c_int32), ("hidden", C.c_int32),
+                ("out_features", C.c_int32), ("heads", C.c_int32), ("scheme_policy", C.c_int32),
+                ("caching", C.c_int32), ("gat_level", C.c_int32), ("leaky_slope", C.c_double),
+                ("input_grad", C.c_int32)]
+
+
 class Scheme(C.Structure):
     _fields_ = [("forward", C.c_int32), ("backward", C.c_int32), ("caching", C.c_int32)]
 
@@ -97,6 +105,11 @@ _SIGS = {
     "sgnn_gat_cache_edge_values": (INT, [VP, VP, VP, VP, VP, VP, VP, VP]),
     "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
                                  VP, VP]),
+    "sgnn_model_create": (INT, [VP, C.POINTER(ModelConfig), U64, INT, PVP]),
+    "sgnn_model_destroy": (INT, [VP]),
+    "sgnn_model_num_params": (INT, [VP, PI32]),
+    "sgnn_model_param": (INT, [VP, I32, PVP, PI64, C.POINTER(C.c_char_p)]),
+    "sgnn_model_train_step": (INT, [VP, VP, VP, VP, VP, VP, VP, PVP, VP, VP]),
     "sgnn_gat_step_host": (INT, [VP, VP, VP, I32, VP, VP, VP, VP, I32, I32, D, INT, INT, VP, INT,
                                  VP, VP, VP, VP, VP, VP]),
 }

@@ -526,3 +526,80 @@ def gat_backward(pattern: Pattern, d_out, theta, a_src, a_dst, cache: GatCache,
                                 int(bool(needs_feature_grad)), _p(d_theta), _p(d_as), _p(d_ad),
                                 _p(d_b), _p(d_x)))
     return d_theta, d_as, d_ad, d_b, d_x
+
+
+# ---- two-layer models (model.hpp:16-245) -----------------------------------------
+class Model:
+    """Gcn2Model / Gat2Model (model.hpp:40-245) over sgnn_model: GCN -> ReLU ->
+    GCN or GAT -> ELU(1) -> GAT.  Parameters live on the device, initialised
+    like the reference constructors (layer 2 from seed+101 / seed+201);
+    `params` are zero-copy views in param_tensors() order (valid while the
+    model lives).  `train_step` is the benchmark step (bench.hpp:193-219):
+    forward, loss_mse against `target`, backward."""
+
+    KINDS = {"gcn2": 0, "gat2": 1}
+
+    def __init__(self, kind, in_features, hidden, out_features, heads=1, scheme="adaptive",
+                 caching=False, gat_level="none", leaky_slope=0.2, input_grad=False, seed=0,
+                 dtype=torch.float32, ctx=None):
+        self.ctx = _ctx(ctx)
+        if kind not in self.KINDS:
+            raise ValueError(f"unknown model kind '{kind}'")
+        if isinstance(scheme, str):
+            if scheme not in _c.POLICIES:
+                raise ValueError("unknown scheme")
+            scheme = _c.POLICIES[scheme]
+        if isinstance(gat_level, str):
+            if gat_level not in _c.LEVELS:
+                raise ValueError(f"unknown caching level '{gat_level}'")
+            gat_level = _c.LEVELS[gat_level]
+        self.kind, self.dtype = kind, dtype
+        self.cfg = _c.ModelConfig(self.KINDS[kind], in_features, hidden, out_features, heads,
+                                  scheme, int(bool(caching)), gat_level, float(leaky_slope),
+                                  int(bool(input_grad)))
+        h = C.c_void_p()
+        check(lib.sgnn_model_create(self.ctx.handle, C.byref(self.cfg), int(seed),
+                                    _DT[dtype], C.byref(h)))
+        self.handle = h
+        m, hid, o = in_features, hidden, out_features
+        shapes = ([(m, hid), (hid,), (hid, o), (o,)] if kind == "gcn2" else
+                  [(m, heads * hid), (heads, hid), (heads, hid), (heads * hid,),
+                   (heads * hid, heads * o), (heads, o), (heads, o), (heads * o,)])
+        cnt = C.c_int32()
+        check(lib.sgnn_model_num_params(h, C.byref(cnt)))
+        ts = {torch.float32: "<f4", torch.float64: "<f8"}[dtype]
+        self.params = []
+        for i in range(cnt.value):
+            ptr, size, name = C.c_void_p(), C.c_int64(), C.c_char_p()
+            check(lib.sgnn_model_param(h, i, C.byref(ptr), C.byref(size), C.byref(name)))
+            t = torch.as_tensor(_CudaArray(ptr.value, size.value, ts), device=self.ctx.device)
+            self.params.append((name.value.decode(), t.view(shapes[i])))
+        self.out_width = o if kind == "gcn2" else heads * o
+
+    def param_tensors(self):
+        return self.params
+
+    def train_step(self, graph, X, target, out=None):
+        """graph: Adjacency (gcn2) or Pattern (gat2).  Returns (loss, out,
+        grads, d_input): loss a device float64 scalar, grads in params order."""
+        X, target = X.contiguous(), target.contiguous()
+        n = X.shape[0]
+        if target.shape != (n, self.out_width):
+            raise ValueError("loss_mse: target shape mismatch")
+        dev = self.ctx.device
+        if out is None:
+            out = torch.empty((n, self.out_width), dtype=self.dtype, device=dev)
+        grads = [torch.empty_like(p) for _, p in self.params]
+        gp = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        d_in = torch.empty_like(X) if self.cfg.input_grad else None
+        loss = torch.zeros((), dtype=torch.float64, device=dev)
+        adj = graph.handle if self.kind == "gcn2" else None
+        pat = graph.handle if self.kind == "gat2" else None
+        check(lib.sgnn_model_train_step(self.ctx.handle, self.handle, adj, pat, _p(X), _p(target),
+                                        _p(out), gp, _p(d_in), _p(loss)))
+        return loss, out, grads, d_in
+
+    def __del__(self, _destroy=lib.sgnn_model_destroy):
+        if getattr(self, "handle", None):
+            _destroy(self.handle)
+            self.handle = None

@@ -190,3 +190,29 @@ def test_gat_layer_all_levels(golden, orc):
         assert np.array_equal(dad, g[f"da_dst_{level}"])
         assert np.array_equal(db, g[f"dbias_{level}"])
         assert np.array_equal(dx, g[f"dinput_{level}"])
+
+
+@pytest.mark.parametrize("tag", ["gcn2_adaptive_cached", "gcn2_adaptive_fg", "gcn2_tf",
+                                 "gat2_h2", "gat2_h8"])
+def test_oracle_model_step_matches_reference(golden, orc, tag):
+    """oracle.gcn2_step / gat2_step (model.hpp restated over the oracle layers)
+    against the reference's own Gcn2Model / Gat2Model step."""
+    g = golden("models")
+    kind, n, seed, m, hid, o, h, pol, ca, lv, ig = (int(x) for x in g[f"{tag}_cfg"])
+    deg = float(g[f"{tag}_deg"][0])
+    _, s, t = orc.synthetic_graph(n, deg, seed)
+    X = orc.random_uniform(n, m, seed + 11)
+    if kind == 0:
+        op = orc.gcn_operator(n, s, t)
+        target = orc.random_uniform(n, o, seed + 12)
+        loss, out, grads, dx = orc.gcn2_step(op, X, orc.gcn2_params(m, hid, o, seed + 13), target,
+                                             pol, bool(ca), bool(ig))
+    else:
+        pat = orc.gat_pattern(n, s, t)
+        target = orc.random_uniform(n, h * o, seed + 12)
+        loss, out, grads, dx = orc.gat2_step(pat, X, orc.gat2_params(m, h, hid, o, seed + 13), h,
+                                             target, 0.2, bool(ig))
+    flat = np.concatenate([np.asarray(x).ravel() for x in grads])
+    assert orc.max_rel_diff(out, g[f"{tag}_pred"]) < 1e-12
+    assert orc.max_rel_diff(flat, g[f"{tag}_grads"]) < 1e-12
+    assert abs(loss - g[f"{tag}_loss"][0]) < 1e-12
