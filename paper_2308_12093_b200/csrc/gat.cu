@@ -571,15 +571,14 @@ static int wgrid(int32_t n) {
     default: { constexpr int RR = 8; __VA_ARGS__; } break; \
   }
 
-// float32 compile-time-heads path (gat_v2.cuh): h in {1,2,4,8}, k/4 a power
-// of two <= 32.  Returns R (16-byte vectors per lane) or 0.
+// float32 compile-time-heads path (gat_v2.cuh): h in {1,2,4,8}, k % 4 == 0,
+// h*k <= 1024.  Returns R (16-byte vectors per lane) or 0.
 template <class T>
 static int v2_R(int32_t h, int32_t k) {
   if (sizeof(T) != 4 || getenv("SGNN_GAT_V1")) return 0;
   if (!(h == 1 || h == 2 || h == 4 || h == 8) || k % 4 != 0) return 0;
-  const int L = k / 4;
-  if ((L & (L - 1)) != 0 || L > 32) return 0;
-  return pick_r(h * k / 4);
+  const int R = pick_r(h * k / 4);
+  return R <= 8 ? R : 0;
 }
 
 // (H, R) -> constexpr instantiation; R <= 32 * H / 32 lanes' worth
@@ -626,7 +625,10 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
   const int R = fast_R<T>(h, k);
   const int R2 = v2_R<T>(h, k);
   if (R2 && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
-    node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+    if (R)
+      node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+    else
+      node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
     const float4* M4 = reinterpret_cast<const float4*>(M.get());
     const float4* b4 = reinterpret_cast<const float4*>(bias);
     float4* o4 = reinterpret_cast<float4*>(out);
@@ -766,8 +768,14 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     }
     const float* al = reinterpret_cast<const float*>(alpha);
     const uint8_t* mk = cached ? c->mask.as<uint8_t>() : mask_t.as<uint8_t>();
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, M4, G4, k,
-                                                                          da.as<float>())));
+    const int L = k / 4;
+    if ((L & (L - 1)) == 0 && L <= 32) {
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<v2_grid(n), 256, 0, st>>>(
+                           n, rp, ci, M4, G4, k, da.as<float>())));
+    } else {
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<v2_grid(n), 256, 0, st>>>(
+                           n, rp, ci, M4, G4, k, da.as<float>())));
+    }
     launched(ctx);
     HR_SWITCH(h, R2, (g2::k_gat_sbwd3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
                          n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),

@@ -471,15 +471,19 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
 // backward, part 1 (kernels.hpp:342-377 semibatched SDDMM): dAlpha[e, t] =
 // <dX'[i, t, :], M[col_e, t, :]>, edge-major.  Lean warp per row: the row of
 // dX' stays in registers, R 16-byte vectors of M gathered per edge, U edges
-// in flight, head-segmented xor reductions over the k/4 lanes of a head.
+// in flight.  P2 (k/4 a power of two <= 32, heads aligned to lane groups):
+// head-segmented xor reductions over the k/4 lanes of a head; otherwise the
+// per-vector partial dots go through shared memory and H*U lanes fold the
+// k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
-template <int H, int R>
+template <int H, int R, bool P2>
 __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                  const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
                  float* __restrict__ da) {
   constexpr int U = R >= 4 ? 1 : 2;
-  const int lane = threadIdx.x & 31;
+  __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     tr[r] = min(H - 1, v / L);
     g[r] = v < fv ? __ldg(G + (int64_t)i * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const bool lead = (lane & (L - 1)) == 0;
+  const bool lead = P2 && (lane & (L - 1)) == 0;
   for (int32_t e = beg; e < end; e += U) {
     uint32_t c[U];
     float4 x[U][R];
@@ -510,13 +514,29 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
       float p[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) p[r] = r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
-      for (int o = L >> 1; o > 0; o >>= 1)
+      if constexpr (P2) {
+        for (int o = L >> 1; o > 0; o >>= 1)
 #pragma unroll
-        for (int r = 0; r < R; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
-      if (lead && e + u < end)
+          for (int r = 0; r < R; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
+        if (lead && e + u < end)
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r * 32 + lane < fv) da[(int64_t)(e + u) * H + tr[r]] = p[r];
+      } else {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (r * 32 + lane < fv) da[(int64_t)(e + u) * H + tr[r]] = p[r];
+          if (r * 32 + lane < fv) sh_p[wib][u][r * 32 + lane] = p[r];
+      }
+    }
+    if constexpr (!P2) {
+      __syncwarp();
+      if (lane < U * H) {
+        const int u = lane / H, t = lane % H;
+        float acc = 0.f;
+        for (int q = 0; q < L; ++q) acc += sh_p[wib][u][t * L + q];
+        if (e + u < end) da[(int64_t)(e + u) * H + t] = acc;
+      }
+      __syncwarp();
     }
   }
 }
@@ -665,7 +685,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
   for (int r = 0; r < R; ++r) {
     const int v = r * 32 + lane;
     if (v < fv) {
-      if ((lane & (L - 1)) == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
+      if (v % L == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
       const float cs = __ldg(dS + (int64_t)j * H + tr[r]);
       const float4 as = __ldg(a_src + v), ad = __ldg(a_dst + v);
       float4 o = acc[r];
