@@ -43,6 +43,7 @@ ARXIV_EDGES = 1166243
 SEED = 1
 M_IN, K_OUT = 128, 256
 GAT_H, GAT_K = 8, 32
+GCN2_HID, GAT2_HID, MODEL_OUT = 256, 32, 40  # config 4 (2-layer models, hidden width 256)
 METRIC = "GCN/GAT layer fwd+bwd ms on OGB-Arxiv shape; SpMM/SDDMM HBM GB/s vs peak"
 
 
@@ -139,6 +140,12 @@ def reference_cpu(steps, warmup, kind=0, cores=None):
     if kind == 0:
         h = L.ref_bench_create(0, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, K_OUT, 1, 1, 0, 1, 0,
                                2)
+    elif kind == 2:  # Gcn2 128-256-40 step, adaptive + caching (config 4)
+        h = L.ref_bench_create(2, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GCN2_HID, 1, 0, 0, 1,
+                               MODEL_OUT << 8, 2)
+    elif kind == 3:  # Gat2 h=8 128-(8x32)-(8x40) step, level full (config 4)
+        h = L.ref_bench_create(3, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GAT2_HID, GAT_H, 0,
+                               0, 0, 3 | (MODEL_OUT << 8), 2)
     else:
         h = L.ref_bench_create(1, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GAT_K, GAT_H, 1, 0,
                                0, 3, 1)
@@ -295,6 +302,22 @@ def run_ours(args):
 
     gat_ms = statistics.mean(timed(gat_step, max(3, args.steps), 2))
 
+    # ---- 2-layer models, full training step with MSE (config 4) -------------
+    gcn2 = d.Model("gcn2", M_IN, GCN2_HID, MODEL_OUT, scheme="adaptive", caching=True,
+                   seed=SEED + 13, ctx=ctx)
+    gat2 = d.Model("gat2", M_IN, GAT2_HID, MODEL_OUT, heads=GAT_H, gat_level="full",
+                   seed=SEED + 13, ctx=ctx)
+    t_gcn2 = d.random_uniform(n, MODEL_OUT, SEED + 12, ctx=ctx)
+    t_gat2 = d.random_uniform(n, GAT_H * MODEL_OUT, SEED + 12, ctx=ctx)
+    gcn2_ms = statistics.mean(timed(lambda: gcn2.train_step(A, X, t_gcn2), max(3, args.steps), 2))
+    gat2_ms = statistics.mean(timed(lambda: gat2.train_step(P, X, t_gat2), max(3, args.steps), 2))
+    models = {"gcn2": {"ms": round(gcn2_ms, 4), "shape": f"{M_IN}-{GCN2_HID}-{MODEL_OUT}",
+                       "relu": True, "caching": True, "scheme": "adaptive"},
+              "gat2": {"ms": round(gat2_ms, 4),
+                       "shape": f"{M_IN}-({GAT_H}x{GAT2_HID})-({GAT_H}x{MODEL_OUT})",
+                       "elu": True, "level": "full"},
+              "loss": "mse vs random_uniform(seed+12)", "input_grad": False}
+
     # ---- e2e through the public API with host buffers -----------------------
     hX = torch.empty((n, M_IN), dtype=torch.float32, pin_memory=True)
     hG = torch.empty((n, K_OUT), dtype=torch.float32, pin_memory=True)
@@ -330,6 +353,14 @@ def run_ours(args):
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+        if not args.no_model_cpu:
+            for kind, key in ((2, "gcn2"), (3, "gat2")):
+                try:
+                    r = reference_cpu(1, 0, kind)
+                    models[key]["reference_cpu_ms"] = round(r["ms"], 1)
+                    models[key]["reference_cpu_cores"] = r["cores"]
+                except Exception as ex:
+                    models[key]["reference_cpu_ms"] = f"unavailable: {ex}"
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -347,6 +378,7 @@ def run_ours(args):
         "breakdown_ms": {k: round(v, 4) for k, v in comps.items()},
         "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K, "level": "full",
                       "nnz": P.nnz},
+        "models": models,
         "setup_s": round(setup_s, 2),
     }
     print(json.dumps(line), flush=True)
@@ -438,6 +470,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-model-cpu", action="store_true",
+                    help="skip the reference's CPU timing of the 2-layer model steps")
     ap.add_argument("--dist", action="store_true",
                     help="use the row-partitioned multi-GPU path even at WORLD_SIZE=1")
     args = ap.parse_args()

@@ -377,7 +377,8 @@ int ref_model_step(int kind, int n, double deg, unsigned long long seed, int m, 
 // CPU timing harness for bench.py (reference arm and cpu_baseline): builds the
 // workload exactly like run_benchmark_typed (bench.hpp:160-219) -- X from
 // seed+11, dX' from seed+12, params from seed+13 -- then times single steps.
-// kind: 0 GCN layer fwd+bwd, 1 GAT layer fwd+bwd. f32 timing like BASELINE.md.
+// kind: 0 GCN layer fwd+bwd, 1 GAT layer fwd+bwd, 2/3 Gcn2/Gat2 training step
+// (k = hidden, level packs the GAT level | out_features << 8). f32 timing.
 // ---------------------------------------------------------------------------
 struct RefBench {
   std::function<void()> step;
@@ -388,6 +389,9 @@ struct RefBench {
   DenseMatrix<float> X, G;
   GcnParams<float> gp;
   GatParams<float> ap;
+  std::optional<Gcn2Model<float>> gcn2;
+  std::optional<Gat2Model<float>> gat2;
+  DenseMatrix<float> target;
 };
 
 void* ref_bench_create(int kind, int n, double deg, unsigned long long seed, int m, int k,
@@ -409,6 +413,47 @@ void* ref_bench_create(int kind, int n, double deg, unsigned long long seed, int
         auto gr = gcn_backward(b->G, *b->adj, b->gp, r.cache, fg != 0);
         (void)gr;
       };
+    } else if (kind >= 2) {
+      // 2-layer model training step (bench.hpp:193-219): m -> hidden (k) -> out,
+      // MSE against random_uniform(seed + 12); kind 2 gcn2, kind 3 gat2 (heads)
+      const int out_f = level >> 8;  // packed: level | out_features << 8
+      ModelConfig mc;
+      mc.kind = kind == 2 ? ModelKind::gcn2 : ModelKind::gat2;
+      mc.in_features = m;
+      mc.hidden = k;
+      mc.out_features = out_f;
+      mc.heads = heads;
+      mc.scheme = static_cast<SchemePolicy>(policy);
+      mc.caching = caching != 0;
+      mc.gat_level = static_cast<GatCacheLevel>(level & 255);
+      mc.input_grad = fg != 0;
+      if (kind == 2) {
+        b->adj.emplace(convert(gcn_normalize(SparseMatrix<float>{adjacency<float>(g)}),
+                               static_cast<SparseFormat>(fmt)));
+        b->q = b->adj->nnz();
+        b->gcn2.emplace(mc, seed + 13);
+        b->target = DenseMatrix<float>::random_uniform(n, out_f, seed + 12);
+        b->step = [b] {
+          typename Gcn2Model<float>::Caches caches;
+          auto o = b->gcn2->forward(b->X, *b->adj, caches);
+          auto l = loss_mse(o, b->target);
+          auto gr = b->gcn2->backward(l.grad, *b->adj, caches);
+          (void)gr;
+        };
+      } else {
+        auto csr = coo_to_csr(to_coo(add_self_loops(SparseMatrix<float>{adjacency<float>(g)})));
+        b->pattern = SparsePattern::from_csr(csr);
+        b->q = b->pattern->nnz();
+        b->gat2.emplace(mc, seed + 13);
+        b->target = DenseMatrix<float>::random_uniform(n, heads * out_f, seed + 12);
+        b->step = [b] {
+          typename Gat2Model<float>::Caches caches;
+          auto o = b->gat2->forward(b->X, b->pattern, caches);
+          auto l = loss_mse(o, b->target);
+          auto gr = b->gat2->backward(l.grad, b->pattern, caches);
+          (void)gr;
+        };
+      }
     } else {
       auto csr = coo_to_csr(to_coo(add_self_loops(SparseMatrix<float>{adjacency<float>(g)})));
       b->pattern = SparsePattern::from_csr(csr);
