@@ -577,7 +577,8 @@ template <class T>
 static int v2_R(int32_t h, int32_t k) {
   if (sizeof(T) != 4 || getenv("SGNN_GAT_V1")) return 0;
   if (!(h == 1 || h == 2 || h == 4 || h == 8) || k % 4 != 0) return 0;
-  const int R = pick_r(h * k / 4);
+  int R = pick_r(h * k / 4);
+  if (h == 8 && R == 4 && h * k / 4 <= 96) R = 3;  // 257..384 wide: 3 vectors per lane
   return R <= 8 ? R : 0;
 }
 
@@ -592,6 +593,7 @@ static int v2_R(int32_t h, int32_t k) {
     case 4 * 16 + 4: { constexpr int HH = 4, RR = 4; __VA_ARGS__; } break;          \
     case 8 * 16 + 1: { constexpr int HH = 8, RR = 1; __VA_ARGS__; } break;          \
     case 8 * 16 + 2: { constexpr int HH = 8, RR = 2; __VA_ARGS__; } break;          \
+    case 8 * 16 + 3: { constexpr int HH = 8, RR = 3; __VA_ARGS__; } break;          \
     case 8 * 16 + 4: { constexpr int HH = 8, RR = 4; __VA_ARGS__; } break;          \
     case 8 * 16 + 8: { constexpr int HH = 8, RR = 8; __VA_ARGS__; } break;          \
     default: throw invalid_argument("gat: no v2 kernel for this head/width");        \
