@@ -25,8 +25,8 @@ def short(name):
     return name.split("(")[0][:70]
 
 
-def launches():
-    rows = list(csv.reader(open(os.path.join(SRC, f"launches_{TAG}.csv"))))
+def launches(name=None):
+    rows = list(csv.reader(open(os.path.join(SRC, name or f"launches_{TAG}.csv"))))
     hdr, data, order = None, {}, []
     for r in rows:
         if "Kernel Name" in r:
@@ -54,6 +54,16 @@ def one_step(ls):
     return steps[5] if len(steps) > 5 else steps[-1]
 
 
+def gat_step(ls):
+    """One GAT layer step of scripts/kbench.py gat: X.Theta GEMM (+ split),
+    node scores, ... up to the next step's GEMM.  Take the last complete one."""
+    idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores" in n]
+    if len(idx) < 2:
+        return []
+    a, b = idx[-2], idx[-1]
+    return ls[a - 2:b - 2]
+
+
 def main():
     ls = launches()
     step = one_step(ls)
@@ -72,7 +82,7 @@ def main():
                "l1tex__throughput.avg.pct_of_peak_sustained_active",
                "sm__throughput.avg.pct_of_peak_sustained_elapsed",
                "sm__warps_active.avg.pct_of_peak_sustained_active",
-               "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+               "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
                "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size"]
     full_rows, traffic = [], {}
     for rep in (f"full_{TAG}", f"full_gat_{TAG}"):
@@ -122,7 +132,28 @@ def main():
         lines.append(f"| {short(n)} | {t / 1e3:.1f} | {t / tot:.1%} | "
                      f"{m.get('dram__bytes_read.sum', 0) / 1e6:.1f} | "
                      f"{m.get('dram__bytes_write.sum', 0) / 1e6:.1f} |")
-    lines += ["", f"step total (serialised): {tot / 1e3:.1f} us", "",
+    lines += ["", f"step total (serialised): {tot / 1e3:.1f} us", ""]
+    gpath = os.path.join(SRC, f"gat_launches_{TAG}.csv")
+    if os.path.exists(gpath):
+        gs = gat_step(launches(f"gat_launches_{TAG}.csv"))
+        gt = sum(m.get("gpu__time_duration.sum", 0) for _, m in gs)
+        lines += ["## One GAT layer step (Arxiv, h=8, k=32, level full, fg)", "",
+                  "| kernel | time us | share | DRAM rd MB | DRAM wr MB |", "|---|---|---|---|---|"]
+        for n, m in gs:
+            t = m.get("gpu__time_duration.sum", 0)
+            lines.append(f"| {short(n)} | {t / 1e3:.1f} | {t / gt:.1%} | "
+                         f"{m.get('dram__bytes_read.sum', 0) / 1e6:.1f} | "
+                         f"{m.get('dram__bytes_write.sum', 0) / 1e6:.1f} |")
+        lines += ["", f"GAT step total (serialised): {gt / 1e3:.1f} us", ""]
+        with open(os.path.join(DST, "gat_step_launches.csv"), "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["kernel", "time_us", "share", "dram_read_MB", "dram_write_MB"])
+            for n, m in gs:
+                t = m.get("gpu__time_duration.sum", 0)
+                w.writerow([short(n), round(t / 1e3, 2), round(t / gt, 4),
+                            round(m.get("dram__bytes_read.sum", 0) / 1e6, 2),
+                            round(m.get("dram__bytes_write.sum", 0) / 1e6, 2)])
+    lines += [
               "## --set full captures (key metrics)", "",
               "(us; DRAM in MB)", "", "| kernel | us | DRAM rd | DRAM wr | DRAM % | L2 % | L1 % | SM % | warps % | tensor pipe % | L2 hit % | regs |",
               "|---|---|---|---|---|---|---|---|---|---|---|---|"]
