@@ -742,7 +742,9 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
   const int64_t q = p->nnz;
   const T beta = (T)c->beta;
   cudaStream_t st = ctx->stream;
-  column_sums<T>(ctx, G, n, hk, d_bias);
+  const int R2 = v2_R<T>(h, k);
+  const bool v2 = R2 && al16(G) && al16(a_src) && al16(a_dst);
+  if (!v2) column_sums<T>(ctx, G, n, hk, d_bias);  // v2: fused with the attention grads
   Recomputed<T> r;
   recompute<T>(ctx, p, c, theta, a_src, a_dst, r);
   const bool cached = c->level == SGNN_GAT_FULL;
@@ -754,8 +756,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     mask_t = DevBuf((size_t)q * h + 8, st);
   }
   const T* alpha = cached ? c->alpha.as<T>() : alpha_t.as<T>();
-  const int R2 = v2_R<T>(h, k);
-  if (R2 && al16(G) && al16(r.Mp) && al16(dM.get()) && al16(a_src) && al16(a_dst)) {
+  if (v2) {  // M, dM come from the 256-byte-aligned pool / cache
     const int32_t* rp = p->rowptr.as<int32_t>();
     const int32_t* ci = p->cols.as<int32_t>();
     const float4* M4 = reinterpret_cast<const float4*>(r.Mp);
@@ -790,19 +791,22 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
                          reinterpret_cast<const float4*>(a_dst), k, dD.as<float>(),
                          reinterpret_cast<float4*>(dM.get()))));
     launched(ctx);
-    constexpr int VW = sizeof(T) == 4 ? 4 : 2;
-    const int32_t chunk = (int32_t)std::max<int64_t>(64, ceil_div(n, ctx->num_sms * 4));
-    const int32_t nch = (int32_t)std::max<int64_t>(1, ceil_div(n, chunk));
-    DevBuf psrc((size_t)nch * hk * 8, st), pdst((size_t)nch * hk * 8, st);
-    gf::k_attgrad2_partial<T, VW><<<nch, 256, 0, st>>>(n, h, k, r.Mp, dS.as<T>(), dD.as<T>(),
-                                                      chunk, psrc.as<double>(), pdst.as<double>());
-    launched(ctx);
-    gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
-                                                                      psrc.as<double>(), d_a_src);
-    launched(ctx);
-    gf::k_reduce_partials<T><<<(unsigned)ceil_div(hk, 32), 256, 0, st>>>(nch, hk,
-                                                                      pdst.as<double>(), d_a_dst);
-    launched(ctx);
+    {  // d_bias, d_a_src, d_a_dst: one pass over dX' and M
+      const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(2 * ctx->num_sms, n));
+      const int32_t chunk = (int32_t)ceil_div(n, nb);
+      DevBuf part((size_t)nb * 3 * hk * sizeof(double), st);
+      switch (h) {
+        case 1: g2::k_grads3_partial<1><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        case 2: g2::k_grads3_partial<2><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        case 4: g2::k_grads3_partial<4><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        default: g2::k_grads3_partial<8><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+      }
+      launched(ctx);
+      g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(
+          nb, hk, part.as<double>(), reinterpret_cast<float*>(d_bias),
+          reinterpret_cast<float*>(d_a_src), reinterpret_cast<float*>(d_a_dst));
+      launched(ctx);
+    }
     gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
             d_theta);
     if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);

@@ -696,4 +696,98 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
   }
 }
 
+// ---------------------------------------------------------------------------
+// backward, part 4: the three column-sum gradients in one pass over the rows
+// (dense.hpp:272-282 column_sums for d_bias = 1^T dX'; kernels.hpp:592-611
+// attention_param_grad for d_a_src = sum_i dS[i,t] M[i,t,:] and d_a_dst with
+// dD).  Block partials in float64, threads own 16-byte column vectors, row
+// groups combined in a fixed order; k_grads3_final folds the partials.
+// part layout: [block][3][hk] (db | d_a_src | d_a_dst, the latter h x k).
+// ---------------------------------------------------------------------------
+template <int H>
+__global__ void __launch_bounds__(256) k_grads3_partial(int32_t n, int32_t k,
+                                                        const float4* __restrict__ G,
+                                                        const float4* __restrict__ M,
+                                                        const float* __restrict__ dS,
+                                                        const float* __restrict__ dD,
+                                                        int32_t chunk, double* __restrict__ part) {
+  __shared__ double sh[3][256][4];
+  const int fv = H * k / 4, L = k / 4;
+  const int groups = max(1, 256 / fv);
+  const int tid = threadIdx.x, v = tid % fv, grp = tid / fv;
+  const int t = min(H - 1, v / L);
+  const int32_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  double a[3][4] = {};
+  if (grp < groups && v < fv) {
+    for (int32_t i = r0 + grp; i < r1; i += groups) {
+      const float4 g = __ldg(G + (int64_t)i * fv + v);
+      const float4 mm = __ldg(M + (int64_t)i * fv + v);
+      const double cs = (double)__ldg(dS + (int64_t)i * H + t);
+      const double cd = (double)__ldg(dD + (int64_t)i * H + t);
+      a[0][0] += g.x;
+      a[0][1] += g.y;
+      a[0][2] += g.z;
+      a[0][3] += g.w;
+      a[1][0] += cs * mm.x;
+      a[1][1] += cs * mm.y;
+      a[1][2] += cs * mm.z;
+      a[1][3] += cs * mm.w;
+      a[2][0] += cd * mm.x;
+      a[2][1] += cd * mm.y;
+      a[2][2] += cd * mm.z;
+      a[2][3] += cd * mm.w;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sh[q][tid][c] = a[q][c];
+  __syncthreads();
+  if (grp == 0 && v < fv) {
+    for (int gg = 1; gg < groups; ++gg)
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[q][c] += sh[q][gg * fv + v][c];
+    double* o = part + (int64_t)blockIdx.x * 3 * fv * 4;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[(int64_t)q * fv * 4 + v * 4 + c] = a[q][c];
+  }
+}
+
+// out[q][c] = sum over blocks of part[b][q][c]; blockIdx.y = q, 32 columns per
+// block, 8 warps x 4 independent chains, fixed-order combine.
+__global__ void __launch_bounds__(256) k_grads3_final(int32_t nb, int32_t hk,
+                                                      const double* __restrict__ part,
+                                                      float* __restrict__ db,
+                                                      float* __restrict__ das,
+                                                      float* __restrict__ dad) {
+  __shared__ double sh[8][33];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = blockIdx.y;
+  const int32_t c = blockIdx.x * 32 + l;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (c < hk) {
+    const double* p = part + (int64_t)q * hk + c;
+    const int64_t st = 3LL * hk;
+    int32_t b = w;
+    for (; b + 24 < nb; b += 32) {
+      s0 += p[b * st];
+      s1 += p[(b + 8) * st];
+      s2 += p[(b + 16) * st];
+      s3 += p[(b + 24) * st];
+    }
+    for (; b < nb; b += 8) s0 += p[b * st];
+  }
+  sh[w][l] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (w == 0 && c < hk) {
+    double t = 0.0;
+#pragma unroll
+    for (int z = 0; z < 8; ++z) t += sh[z][l];
+    (q == 0 ? db : q == 1 ? das : dad)[c] = (float)t;
+  }
+}
+
 }  // namespace g2
