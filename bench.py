@@ -290,6 +290,16 @@ def run_ours(args):
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                 "traffic": _traffic(dominant), "algorithmic_bytes": dom_bytes, "peak_source": peak_kind,
                 "ms": round(comps[dominant], 4)}
+    if dominant.startswith("spmm"):
+        # the SpMM gathers one dense row per edge: q' * 512 B of L2->SM traffic;
+        # ceiling = the chip's random 512 B row-gather rate at this table size
+        # (scripts/gather_probe.cu, profiles/r1/gather_probe.txt: 86.7 MB table)
+        gathered = q * M_IN * 4
+        g_gbs = gathered / (comps[dominant] * 1e-3) / 1e9
+        roofline["gather"] = {"gathered_bytes": gathered, "achieved": round(g_gbs, 1),
+                              "probe_peak": 11118.0, "unit": "GB/s",
+                              "frac": round(g_gbs / 11118.0, 4),
+                              "source": "profiles/r1/gather_probe.txt"}
 
     # ---- GAT layer (h=8, k=32, cache level full) on the same graph ----------
     Xg = X
