@@ -154,7 +154,17 @@ template void gemm_simt<double>(sgnn_ctx, const double*, int32_t, int32_t, const
 // tcgen05 path (gemm_tc.cu); returns false when the shape is not supported
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
-                 float* colsum_b);
+                 float* colsum_b, const float* att_src = nullptr, const float* att_dst = nullptr,
+                 float* s_out = nullptr, float* d_out = nullptr, int heads = 0);
+
+// M = X Theta with the GAT node scores s, d (n x h) computed in the GEMM
+// epilogue; false when the fused form does not apply (nothing done)
+bool gemm_scores_f32(sgnn_ctx ctx, const float* X, int32_t n, int32_t m, const float* theta,
+                     int32_t hk, float* M, const float* a_src, const float* a_dst, int32_t h,
+                     float* s, float* d) {
+  return gemm_tc_f32(ctx, X, n, m, theta, m, hk, false, false, M, nullptr, nullptr, a_src, a_dst,
+                     s, d, h);
+}
 
 template <>
 void gemm<float>(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,

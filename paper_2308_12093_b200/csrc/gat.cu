@@ -621,16 +621,24 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
   cudaStream_t st = ctx->stream;
   DevBuf M((size_t)n * hk * sizeof(T), st), s((size_t)n * h * sizeof(T) + 8, st),
       d((size_t)n * h * sizeof(T) + 8, st), alpha, mask;
-  gemm<T>(ctx, X, n, m, theta, m, hk, false, false, M.as<T>());
   const int32_t* rp = p->rowptr.as<int32_t>();
   const int32_t* ci = p->cols.as<int32_t>();
   const int R = fast_R<T>(h, k);
   const int R2 = v2_R<T>(h, k);
-  if (R2 && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
-    if (R)
+  const bool v2 = R2 && al16(out) && al16(bias) && al16(a_src) && al16(a_dst);
+  bool scored = false;  // node scores fused into the X.Theta epilogue (k % 32 == 0)
+  if constexpr (sizeof(T) == 4)
+    if (v2)
+      scored = gemm_scores_f32(ctx, X, n, m, theta, hk, M.as<float>(), a_src, a_dst, h,
+                               s.as<float>(), d.as<float>());
+  if (!scored) gemm<T>(ctx, X, n, m, theta, m, hk, false, false, M.as<T>());
+  if (v2) {
+    if (scored) {
+    } else if (R) {
       node_scores_fast<T>(ctx, R, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
-    else
+    } else {
       node_scores<T>(ctx, n, h, k, M.as<T>(), a_src, a_dst, s.as<T>(), d.as<T>());
+    }
     const float4* M4 = reinterpret_cast<const float4*>(M.get());
     const float4* b4 = reinterpret_cast<const float4*>(bias);
     float4* o4 = reinterpret_cast<float4*>(out);
@@ -712,9 +720,25 @@ static void recompute(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* t
     r.Mp = c->M.as<T>();
   } else {
     r.M = DevBuf((size_t)n * hk * sizeof(T), st);
-    gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, c->m, theta, c->m, hk, false, false,
-            r.M.template as<T>());
+    bool scored = false;
+    if constexpr (sizeof(T) == 4) {  // level none: M and s, d from one GEMM
+      if (v2_R<T>(h, k) && al16(a_src) && al16(a_dst)) {
+        r.s = DevBuf((size_t)n * h * sizeof(T) + 8, st);
+        r.d = DevBuf((size_t)n * h * sizeof(T) + 8, st);
+        scored = gemm_scores_f32(ctx, static_cast<const float*>(c->saved_input), n, c->m, theta,
+                                 hk, r.M.template as<float>(), a_src, a_dst, h,
+                                 r.s.template as<float>(), r.d.template as<float>());
+      }
+    }
+    if (!scored)
+      gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, c->m, theta, c->m, hk, false, false,
+              r.M.template as<T>());
     r.Mp = r.M.template as<T>();
+    if (scored) {
+      r.sp = r.s.template as<T>();
+      r.dp = r.d.template as<T>();
+      return;
+    }
   }
   if (c->level == SGNN_GAT_FULL) return;
   if (c->level == SGNN_GAT_NODE_ATTENTION) {

@@ -188,6 +188,16 @@ __global__ void k_split_global(int64_t n, const float* __restrict__ x, float* __
   }
 }
 
+// optional epilogue: GAT node scores s = M a_src^T, d = M a_dst^T per head
+// (kernels.hpp:385-423) from the output tile while it is in registers
+struct EpiScores {
+  const float* a_src = nullptr;
+  const float* a_dst = nullptr;
+  float* s = nullptr;
+  float* d = nullptr;
+  int h = 0, k = 0;
+};
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;  // 16 KB raw A tile
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
               int M, int N, int K, int kchunk, int splits, float* __restrict__ C, int ldc,
               const float* __restrict__ bias, float* __restrict__ part, int tma_store,
-              float* __restrict__ cs_part) {
+              float* __restrict__ cs_part, const EpiScores sc) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
   constexpr int NA = CF::NA;
@@ -477,10 +487,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[abuf], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = m0 + q * 32 + lane;
+      float ss = 0.f, sd = 0.f;  // fused node scores of the current head
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
+        if (sc.a_src != nullptr && n0 + c < N) {
+          // s[i,t] = sum_c a_src[t,c] M[i,tk+c] (kernels.hpp:385-423): a_src is h x k
+          // row-major, so its flat index is the output column; k % 32 == 0 and
+          // BN % k == 0, so a head is whole within this tile
+          const int col0 = n0 + c;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float mv = __uint_as_float(r[j]);
+            ss = fmaf(mv, __ldg(sc.a_src + col0 + j), ss);
+            sd = fmaf(mv, __ldg(sc.a_dst + col0 + j), sd);
+          }
+          if ((col0 + 32) % sc.k == 0) {
+            if (row < M) {
+              sc.s[(int64_t)row * sc.h + col0 / sc.k] = ss;
+              sc.d[(int64_t)row * sc.h + col0 / sc.k] = sd;
+            }
+            ss = sd = 0.f;
+          }
+        }
         if (tma_store) {
           // stage the 32 x 32 block in smem (SWIZZLE_128B: 16 B chunk j of row
           // `lane` at chunk j ^ (lane & 7), conflict-free) and let TMA write
@@ -645,7 +675,8 @@ struct Maps {
 
 template <bool A_MN, bool B_MN, int BN, bool B_PRE>
 static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits, int kchunk,
-                   float* C, const float* bias, float* part, int tma_store, float* cs_part) {
+                   float* C, const float* bias, float* part, int tma_store, float* cs_part,
+                   const EpiScores& sc) {
   auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE>;
   const int smem = Cfg<BN>::SMEM;
   static bool attr_set = false;  // per instantiation
@@ -656,16 +687,17 @@ static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits
   const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * splits;
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
   kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(mp.a, mp.b, mp.blo, mp.c, M, N, K, kchunk,
-                                                  splits, C, N, bias, part, tma_store, cs_part);
+                                                  splits, C, N, bias, part, tma_store, cs_part,
+                                                  sc);
   launched(ctx);
 }
 
 template <int BN>
 static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& mp, int M, int N,
                      int K, int splits, int kchunk, float* C, const float* bias, float* part,
-                     int tma_store, float* cs_part) {
+                     int tma_store, float* cs_part, const EpiScores& sc) {
 #define L(AM, BM_, PR) \
-  launch<AM, BM_, BN, PR>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part)
+  launch<AM, BM_, BN, PR>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc)
   if (pre) {
     if (a_mn && b_mn) L(true, true, true);
     else if (a_mn) L(true, false, true);
@@ -699,7 +731,8 @@ static bool tc_disabled() {
 // fused form does not apply (the caller then runs the two ops separately).
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
-                 float* colsum_b) {
+                 float* colsum_b, const float* att_src, const float* att_dst, float* s_out,
+                 float* d_out, int heads) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
@@ -744,6 +777,19 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   }
   const int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
   splits = (int)ceil_div(K, kchunk);
+  EpiScores sc;
+  if (att_src) {  // fused node scores: whole heads per tile, no split-K, no bias
+    const int hk = heads > 0 ? N / heads : 0;
+    if (splits != 1 || bias || heads <= 0 || hk * heads != N || hk % 32 != 0 || BN % hk != 0 ||
+        (reinterpret_cast<uintptr_t>(att_src) & 15) || (reinterpret_cast<uintptr_t>(att_dst) & 15))
+      return false;
+    sc.a_src = att_src;
+    sc.a_dst = att_dst;
+    sc.s = s_out;
+    sc.d = d_out;
+    sc.h = heads;
+    sc.k = hk;
+  }
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
   const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));
   if (!tma_store) mp.c = mp.a;  // unused
@@ -764,9 +810,9 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     cs = csp.as<float>();
   }
   switch (BN) {
-    case 32: dispatch<32>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
-    case 64: dispatch<64>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
-    default: dispatch<128>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs); break;
+    case 32: dispatch<32>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
+    case 64: dispatch<64>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
+    default: dispatch<128>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
   }
   if (splits > 1) {
     const int64_t MN = (int64_t)M * N;

@@ -65,6 +65,12 @@ void destroy_pipe(sgnn_ctx ctx);
 
 void build_ptr(sgnn_ctx ctx, const int32_t* sorted_ids, int64_t nnz, int32_t n, int32_t* ptr);
 
+// M = X Theta (tcgen05) with the GAT node scores fused into the epilogue;
+// returns false (nothing launched) when the shape does not allow it
+bool gemm_scores_f32(sgnn_ctx ctx, const float* X, int32_t n, int32_t m, const float* theta,
+                     int32_t hk, float* M, const float* a_src, const float* a_dst, int32_t h,
+                     float* s, float* d);
+
 // C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
