@@ -656,7 +656,7 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
       alpha_tmp = DevBuf((size_t)q * h * sizeof(T) + 16, st);
       ap = alpha_tmp.as<float>();
     }
-    HR_SWITCH(h, R2, (g2::k_gat_attn3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+    HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, ci, sp, dp, (float)beta, ap, mp)));
     launched(ctx);
     HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, ap, M4, k,
@@ -788,7 +788,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const float* sp = reinterpret_cast<const float*>(r.sp);
     const float* dp = reinterpret_cast<const float*>(r.dp);
     if (!cached) {  // attention + mask recomputed like gat_recompute (gat.hpp:150-170)
-      HR_SWITCH(h, R2, (g2::k_gat_attn3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+      HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                            n, rp, ci, sp, dp, (float)beta, alpha_t.as<float>(),
                            mask_t.as<uint8_t>())));
       launched(ctx);
@@ -804,7 +804,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
                            n, rp, ci, M4, G4, k, da.as<float>())));
     }
     launched(ctx);
-    HR_SWITCH(h, R2, (g2::k_gat_sbwd3<HH><<<g2::attn3_grid(n), 256, 0, st>>>(
+    HR_SWITCH(h, R2, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
                          dS.as<float>())));
     launched(ctx);

@@ -790,4 +790,180 @@ __global__ void __launch_bounds__(256) k_grads3_final(int32_t nb, int32_t hk,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sub-warp variants of the attention and softmax-backward kernels: a group of
+// GS = 16 lanes owns a row (2 rows per warp), lanes over the row's edges, so
+// the per-edge vectors (d rows, alpha, dAlpha, dy, mask: h values each) are
+// read and written as contiguous, coalesced spans.  Group reductions are the
+// transposed butterfly of allreduce() restricted to the 16 lanes; loops run a
+// warp-uniform trip count (the longer of the two rows) so every shuffle has
+// all lanes.
+// ---------------------------------------------------------------------------
+constexpr int GS = 16;
+
+template <int H, class Op>
+__device__ __forceinline__ void group_allreduce(float (&v)[H], int gl, Op op) {
+  constexpr int LG = Log2<H>::v;
+#pragma unroll
+  for (int st = 0; st < LG; ++st) {
+    const int o = (GS / 2) >> st;
+    const int half = H >> (st + 1);
+    const bool up = (gl & o) != 0;
+#pragma unroll
+    for (int q = 0; q < half; ++q) {
+      const float send = up ? v[q] : v[q + half];
+      const float keep = up ? v[q + half] : v[q];
+      v[q] = op(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+#pragma unroll
+  for (int o = (GS / 2) >> LG; o > 0; o >>= 1)
+    v[0] = op(v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+  const float mine = v[0];
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    int src = 0;
+#pragma unroll
+    for (int st = 0; st < LG; ++st)
+      if (t & (H >> (st + 1))) src |= (GS / 2) >> st;
+    v[t] = __shfl_sync(0xffffffffu, mine, src, GS);
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const int32_t* __restrict__ cols,
+                                                   const float* __restrict__ s,
+                                                   const float* __restrict__ d, float beta,
+                                                   float* __restrict__ alpha,
+                                                   uint8_t* __restrict__ mask) {
+  const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
+  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
+  int32_t beg = 0, end = 0;
+  if (i < n) {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+  }
+  const int32_t deg = end - beg;
+  const int32_t wdeg = max(deg, __shfl_xor_sync(0xffffffffu, deg, GS));  // warp-uniform
+  if (wdeg == 0) return;
+  float si[H];
+  if (i < n) ld_heads<H>(s + (int64_t)i * H, si);
+  float w[H], mx[H], sm[H];
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    mx[t] = -INFINITY;
+    sm[t] = 0.f;
+  }
+  for (int32_t off = 0; off < wdeg; off += GS) {  // max
+    const int32_t e = beg + off + gl;
+    if (off + gl < deg) {
+      float dj[H];
+      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        w[t] = lrelu(si[t] + dj[t], beta);
+        mx[t] = fmaxf(mx[t], w[t]);
+      }
+    }
+  }
+  group_allreduce<H>(mx, gl, OpMax());
+  const bool one = wdeg <= GS;  // the lane's scores are still in w[]
+  for (int32_t off = 0; off < wdeg; off += GS) {  // sum
+    const int32_t e = beg + off + gl;
+    if (off + gl < deg) {
+      if (!one) {
+        float dj[H];
+        ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+        for (int t = 0; t < H; ++t) w[t] = lrelu(si[t] + dj[t], beta);
+      }
+#pragma unroll
+      for (int t = 0; t < H; ++t) sm[t] += __expf(w[t] - mx[t]);
+    }
+  }
+  group_allreduce<H>(sm, gl, OpSum());
+#pragma unroll
+  for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
+  for (int32_t off = 0; off < wdeg; off += GS) {  // alpha, mask
+    const int32_t e = beg + off + gl;
+    if (off + gl < deg) {
+      float dj[H], a[H];
+      uint32_t pos = 0;
+      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        const float y = si[t] + dj[t];
+        if (y > 0.f) pos |= 1u << t;
+        a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+      }
+      st_heads<H>(alpha + (int64_t)e * H, a);
+      if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const float* __restrict__ alpha,
+                                                   const uint8_t* __restrict__ mask,
+                                                   const float* __restrict__ da, float beta,
+                                                   float* __restrict__ dy,
+                                                   float* __restrict__ dS) {
+  const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
+  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
+  int32_t beg = 0, end = 0;
+  if (i < n) {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+  }
+  const int32_t deg = end - beg;
+  const int32_t wdeg = max(deg, __shfl_xor_sync(0xffffffffu, deg, GS));
+  if (wdeg == 0) {
+    if (i < n && gl == 0) {
+      float z[H];
+#pragma unroll
+      for (int t = 0; t < H; ++t) z[t] = 0.f;
+      st_heads<H>(dS + (int64_t)i * H, z);
+    }
+    return;
+  }
+  float a[H], g[H], dot[H], rs[H];
+#pragma unroll
+  for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
+  for (int32_t off = 0; off < wdeg; off += GS) {
+    const int32_t e = beg + off + gl;
+    if (off + gl < deg) {
+      ld_heads<H>(alpha + (int64_t)e * H, a);
+      ld_heads<H>(da + (int64_t)e * H, g);
+#pragma unroll
+      for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
+    }
+  }
+  group_allreduce<H>(dot, gl, OpSum());
+  const bool one = wdeg <= GS;  // a[], g[] still hold the lane's edge
+  for (int32_t off = 0; off < wdeg; off += GS) {
+    const int32_t e = beg + off + gl;
+    if (off + gl < deg) {
+      if (!one) {
+        ld_heads<H>(alpha + (int64_t)e * H, a);
+        ld_heads<H>(da + (int64_t)e * H, g);
+      }
+      const uint32_t pos = ld_mask<H>(mask + (int64_t)e * H);
+      float y[H];
+#pragma unroll
+      for (int t = 0; t < H; ++t) {
+        const float dw = a[t] * (g[t] - dot[t]);
+        y[t] = (pos >> t) & 1u ? dw : beta * dw;
+        rs[t] += y[t];
+      }
+      st_heads<H>(dy + (int64_t)e * H, y);
+    }
+  }
+  group_allreduce<H>(rs, gl, OpSum());
+  if (i < n && gl == 0) st_heads<H>(dS + (int64_t)i * H, rs);
+}
+
+static inline unsigned sub_grid(int32_t n) { return (unsigned)((n + 256 / GS - 1) / (256 / GS)); }
+
 }  // namespace g2
