@@ -374,7 +374,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators, device-side)",
         "config": dict(_config(), scheme=str(scheme), nnz=q),
         "roofline": roofline,
@@ -405,6 +405,9 @@ def run_ours_dist(args):
     import torch
     import torch.distributed as dist
 
+    for key, val in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                     ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533")):
+        os.environ.setdefault(key, val)  # --dist at one GPU without torchrun
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -432,13 +435,16 @@ def run_ours_dist(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
-        out, cache = layer.forward(X, theta, bias, scheme)
+        # layer-1 input features are static across steps: gathered once
+        # (SURVEY 8(e)); the output gradient's propagation is exchanged every step
+        out, cache = layer.forward(X, theta, bias, scheme, static_input=True)
         return layer.backward(G, theta, cache, True)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    launches0 = ctx.launch_count
     ms = []
     with Clocks(local) as clk:
         for _ in range(args.steps):
@@ -452,9 +458,45 @@ def run_ours_dist(args):
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
+    launches = (ctx.launch_count - launches0) // max(1, args.steps)
     t = torch.tensor([sum(ms) / len(ms)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     mean_ms = float(t.item())
+
+    # e2e: each rank's row block of X and dX' from pinned host memory, the
+    # rank's rows of out / dX and (rank 0) dTheta / db back to the host
+    hX, hG = X.cpu().pin_memory(), G.cpu().pin_memory()
+    h_out = torch.empty((r1 - r0, K_OUT), dtype=torch.float32).pin_memory()
+    h_dx = torch.empty((r1 - r0, M_IN), dtype=torch.float32).pin_memory()
+    h_dth = torch.empty((M_IN, K_OUT), dtype=torch.float32).pin_memory()
+    h_db = torch.empty(K_OUT, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        Xd, Gd = hX.to(dev, non_blocking=True), hG.to(dev, non_blocking=True)
+        out, cache = layer.forward(Xd, theta, bias, scheme)
+        h_out.copy_(out, non_blocking=True)
+        dth, db, dx = layer.backward(Gd, theta, cache, True)
+        h_dx.copy_(dx, non_blocking=True)
+        h_dth.copy_(dth, non_blocking=True)
+        h_db.copy_(db, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    ems = []
+    for _ in range(max(3, args.steps)):
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(ems) / len(ems)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    h2d = (hX.numel() + hG.numel()) * 4 * world
+    d2h = (h_out.numel() + h_dx.numel()) * 4 * world + (h_dth.numel() + h_db.numel()) * 4
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(mean_ms, 4), "unit": "ms", "n_gpus": world,
@@ -464,6 +506,10 @@ def run_ours_dist(args):
             "config": dict(_config(), scheme=str(s), nnz=int(r.numel()),
                            parallelism=f"row-partition x{world} (NCCL all-gather/all-reduce)"),
             "clocks": clk.summary(),
+            "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": None, "cpu_baseline": None,
             "edges_per_s": round(int(r.numel()) / (mean_ms * 1e-3), 1),
             "rows_per_rank": [layer.bounds[p + 1] - layer.bounds[p] for p in range(world)],
         }

@@ -202,6 +202,12 @@ int sgnn_edge_softmax(sgnn_ctx ctx, sgnn_pattern p, int32_t heads, const void* w
 /* dense.hpp:97-157 gemm: C = op(A) op(B); A is ra x ca, B is rb x cb */
 int sgnn_gemm(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
               int32_t rb, int32_t cb, int trans_a, int trans_b, void* C);
+/* gemm with the bias add fused into the epilogue (dense.hpp:159-170), or --
+ * for C = A^T B -- with colsum_b = 1^T B computed from the same read of B
+ * (d_bias fused into dTheta, gcn.hpp:139-141); either extra may be NULL */
+int sgnn_gemm_ex(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+                 int32_t rb, int32_t cb, int trans_a, int trans_b, void* C, const void* bias,
+                 void* colsum_b);
 /* dense.hpp:272-282 column_sums: out (cols) = sum over rows */
 int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
                      void* out);

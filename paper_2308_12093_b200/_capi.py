@@ -92,6 +92,7 @@ _SIGS = {
     "sgnn_sddmm": (INT, [VP, VP, VP, I32, VP, I32, INT, VP]),
     "sgnn_edge_softmax": (INT, [VP, VP, I32, VP, INT, VP]),
     "sgnn_gemm": (INT, [VP, INT, VP, I32, I32, VP, I32, I32, INT, INT, VP]),
+    "sgnn_gemm_ex": (INT, [VP, INT, VP, I32, I32, VP, I32, I32, INT, INT, VP, VP, VP]),
     "sgnn_column_sums": (INT, [VP, INT, VP, I32, I32, VP]),
     "sgnn_gcn_forward": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, PVP]),
     "sgnn_gcn_backward": (INT, [VP, VP, VP, VP, I32, I32, VP, INT, VP, VP, VP]),

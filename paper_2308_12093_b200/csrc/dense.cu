@@ -393,6 +393,23 @@ int sgnn_gemm(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, co
   SGNN_API_END
 }
 
+int sgnn_gemm_ex(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+                 int32_t rb, int32_t cb, int ta, int tb, void* C, const void* bias,
+                 void* colsum_b) {
+  SGNN_API_BEGIN
+  if (colsum_b) {
+    require(ta != 0 && tb == 0 && bias == nullptr, "gemm: colsum_b needs C = A^T B, no bias");
+    DISPATCH_T(dtype, gemm_tn_colsum<T>(ctx, static_cast<const T*>(A), ra, ca,
+                                        static_cast<const T*>(B), rb, cb, static_cast<T*>(C),
+                                        static_cast<T*>(colsum_b)));
+  } else {
+    DISPATCH_T(dtype, gemm<T>(ctx, static_cast<const T*>(A), ra, ca, static_cast<const T*>(B), rb,
+                              cb, ta != 0, tb != 0, static_cast<T*>(C),
+                              static_cast<const T*>(bias)));
+  }
+  SGNN_API_END
+}
+
 int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
                      void* out) {
   SGNN_API_BEGIN

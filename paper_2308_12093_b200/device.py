@@ -315,14 +315,22 @@ class Pattern:
 
 
 # ---- kernels -----------------------------------------------------------------
-def gemm(A, B, trans_a=False, trans_b=False, ctx=None):
+def gemm(A, B, trans_a=False, trans_b=False, ctx=None, bias=None, out=None, colsum_b=None):
+    """C = op(A) op(B) (+ bias fused); colsum_b (for A^T B): also 1^T B from
+    the same read of B.  `out` may be a preallocated (e.g. strided-row) view."""
     ctx = _ctx(ctx)
     A, B = A.contiguous(), B.contiguous()
     m = A.shape[1] if trans_a else A.shape[0]
     n = B.shape[0] if trans_b else B.shape[1]
-    out = torch.empty((m, n), dtype=A.dtype, device=A.device)
-    check(lib.sgnn_gemm(ctx.handle, _dt(A), _p(A), A.shape[0], A.shape[1], _p(B), B.shape[0],
-                        B.shape[1], int(trans_a), int(trans_b), _p(out)))
+    if out is None:
+        out = torch.empty((m, n), dtype=A.dtype, device=A.device)
+    if bias is None and colsum_b is None:
+        check(lib.sgnn_gemm(ctx.handle, _dt(A), _p(A), A.shape[0], A.shape[1], _p(B),
+                            B.shape[0], B.shape[1], int(trans_a), int(trans_b), _p(out)))
+    else:
+        check(lib.sgnn_gemm_ex(ctx.handle, _dt(A), _p(A), A.shape[0], A.shape[1], _p(B),
+                               B.shape[0], B.shape[1], int(trans_a), int(trans_b), _p(out),
+                               _p(bias), _p(colsum_b)))
     return out
 
 

@@ -78,12 +78,16 @@ class DeviceOps:
         return d.Adjacency(n_rows, n_cols, t(rows, torch.int32), t(cols, torch.int32),
                            t(vals, dtype), "csr")
 
+    def empty(self, rows, cols, dtype):
+        return torch.empty((rows, cols), dtype=dtype, device=self.dev)
+
     def spmm(self, adj, B, bias=None):
         return adj.spmm(B.contiguous(), bias=bias)
 
-    def gemm(self, A, B, ta=False, tb=False, bias=None):
-        out = self.d.gemm(A, B, ta, tb)
-        return out if bias is None else out + bias
+    def gemm(self, A, B, ta=False, tb=False, bias=None, out=None, colsum_b=None):
+        """bias fused into the epilogue; colsum_b = 1^T B from the same read
+        of B (C = A^T B); out may be a row range of a larger buffer."""
+        return self.d.gemm(A, B, ta, tb, bias=bias, out=out, colsum_b=colsum_b)
 
     def colsum(self, X):
         return self.d.column_sums(X)
@@ -113,12 +117,28 @@ def all_reduce_sum(t, group=None):
 # ---------------------------------------------------------------------------
 # partitioned GCN layer (gcn.hpp:91-193 over row blocks)
 # ---------------------------------------------------------------------------
+def padded_columns(cols, bounds, mx):
+    """Global column j -> owner(j) * mx + (j - bounds[owner]): the row of j in
+    the padded all-gather layout (world blocks of mx rows).  Monotonic in j,
+    so the stored (ascending-column) order of every row is unchanged."""
+    cols = np.asarray(cols, np.int64)
+    b = np.asarray(bounds, np.int64)
+    owner = np.searchsorted(b, cols, side="right") - 1
+    return (owner * mx + (cols - b[owner])).astype(np.int32)
+
+
 class DistGcnLayer:
     """One GCN layer over a row-partitioned normalized operator.
 
     rows/cols/vals: the full canonical normalized COO of A' (host arrays; every
     rank builds only its blocks).  scheme: (forward, backward, caching) ints of
     the reference's SchemeChoice (resolve with device.resolve_scheme).
+
+    Gathered operands use a padded layout -- world blocks of mx = max block
+    rows -- and the local operator blocks index it directly (their column ids
+    are remapped once at setup), so a rank's producer (GEMM) writes its rows
+    straight into its slot of the gather buffer and the all-gather is
+    in place: no pad or concatenation copies, and none at all at world 1.
     """
 
     def __init__(self, n, rows, cols, vals, ops, dtype=torch.float32, group=None):
@@ -131,50 +151,95 @@ class DistGcnLayer:
         self.n = n
         self.bounds = partition_rows(rowptr, self.world)
         self.r0, self.r1 = self.bounds[self.rank], self.bounds[self.rank + 1]
-        self.ops = ops
+        self.mx = max(self.bounds[p + 1] - self.bounds[p] for p in range(self.world))
+        self.ops, self.dtype = ops, dtype
         nl = self.r1 - self.r0
-        self.A = ops.adjacency(nl, n, *row_block(rows, cols, vals, self.r0, self.r1), dtype)
-        self.AT = ops.adjacency(nl, n, *transposed_block(rows, cols, vals, self.r0, self.r1),
-                                dtype)
+        wide = self.world * self.mx
+        r, c, v = row_block(rows, cols, vals, self.r0, self.r1)
+        self.A = ops.adjacency(nl, wide, r, padded_columns(c, self.bounds, self.mx), v, dtype)
+        r, c, v = transposed_block(rows, cols, vals, self.r0, self.r1)
+        self.AT = ops.adjacency(nl, wide, r, padded_columns(c, self.bounds, self.mx), v, dtype)
+        self._static = None
 
-    def forward(self, X_local, theta, bias, scheme):
+    # -- padded in-place all-gather ------------------------------------------
+    def _buffer(self, f, dtype):
+        buf = self.ops.empty(self.world * self.mx, f, dtype)
+        lo = self.rank * self.mx
+        return buf, buf[lo: lo + (self.r1 - self.r0)]
+
+    def _exchange(self, buf):
+        if self.world > 1:
+            lo = self.rank * self.mx
+            dist.all_gather_into_tensor(buf, buf[lo: lo + self.mx], group=self.group)
+        return buf
+
+    def gather(self, local):
+        """Every rank's row block of `local`, padded layout."""
+        buf, mine = self._buffer(local.shape[1], local.dtype)
+        mine.copy_(local)
+        return self._exchange(buf)
+
+    def gather_static(self, X_local):
+        """Layer-1 input features are the same every step: gather them once
+        ('free for layer 1, replicate once')."""
+        self._static = self.gather(X_local)
+        return self._static
+
+    def _allreduce(self, *ts):
+        if self.world == 1:
+            return ts
+        flat = torch.cat([t.reshape(-1) for t in ts])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        out, o = [], 0
+        for t in ts:
+            out.append(flat[o: o + t.numel()].view_as(t))
+            o += t.numel()
+        return tuple(out)
+
+    def forward(self, X_local, theta, bias, scheme, static_input=False):
         fwd = scheme[0]
         ops = self.ops
         cache = {"scheme": scheme}
-        if fwd == 0:  # transform-first: M = X Theta, gather M, out = A'_p M + b
-            M_local = ops.gemm(X_local, theta)
-            M = all_gather_rows(M_local, self.bounds, self.group)
-            out = ops.spmm(self.A, M, bias)
+        if fwd == 0:  # transform-first: M = X Theta into my slot, gather, out = A'_p M + b
+            buf, mine = self._buffer(theta.shape[1], X_local.dtype)
+            ops.gemm(X_local, theta, out=mine)
+            out = ops.spmm(self.A, self._exchange(buf), bias)
             cache["X"] = X_local
         else:  # propagate-first: gather X, P_p = A'_p X, out = P_p Theta + b
-            X = all_gather_rows(X_local, self.bounds, self.group)
+            if static_input:
+                X = self._static if self._static is not None else self.gather_static(X_local)
+            else:
+                X = self.gather(X_local)
             P = ops.spmm(self.A, X)
             out = ops.gemm(P, theta, bias=bias)
             if fwd == 2:
                 cache["P"] = P
             else:
                 cache["X"] = X_local
+                cache["Xg"] = X if static_input else None
         return out, cache
 
     def backward(self, G_local, theta, cache, needs_feature_grad):
         ops = self.ops
         bwd = cache["scheme"][1]
-        d_bias = all_reduce_sum(ops.colsum(G_local), self.group)
         d_input = None
         if bwd == 0:  # fused: S = A'^T G (rows of my block), dTheta = X^T S
-            G = all_gather_rows(G_local, self.bounds, self.group)
-            S = ops.spmm(self.AT, G)
-            d_theta = all_reduce_sum(ops.gemm(cache["X"], S, ta=True), self.group)
+            d_bias = ops.colsum(G_local)
+            S = ops.spmm(self.AT, self.gather(G_local))
+            d_theta, d_bias = self._allreduce(ops.gemm(cache["X"], S, ta=True), d_bias)
             if needs_feature_grad:
                 d_input = ops.gemm(S, theta, tb=True)
         else:
             if bwd == 1:  # split: recompute P_p = A'_p X
-                X = all_gather_rows(cache["X"], self.bounds, self.group)
-                P = ops.spmm(self.A, X)
+                X = cache.get("Xg")
+                P = ops.spmm(self.A, X if X is not None else self.gather(cache["X"]))
             else:
                 P = cache["P"]
-            d_theta = all_reduce_sum(ops.gemm(P, G_local, ta=True), self.group)
+            d_bias = ops.empty(1, G_local.shape[1], G_local.dtype).view(-1)
+            d_theta = ops.gemm(P, G_local, ta=True, colsum_b=d_bias)
+            d_theta, d_bias = self._allreduce(d_theta, d_bias)
             if needs_feature_grad:
-                G2 = all_gather_rows(ops.gemm(G_local, theta, tb=True), self.bounds, self.group)
-                d_input = ops.spmm(self.AT, G2)
+                buf, mine = self._buffer(theta.shape[0], G_local.dtype)
+                ops.gemm(G_local, theta, tb=True, out=mine)
+                d_input = ops.spmm(self.AT, self._exchange(buf))
         return d_theta, d_bias, d_input

@@ -36,11 +36,21 @@ class CpuOps:
         t = torch.from_numpy(out)
         return t if bias is None else t + bias
 
-    def gemm(self, A, B, ta=False, tb=False, bias=None):
+    def empty(self, rows, cols, dtype):
+        return torch.empty((rows, cols), dtype=dtype)
+
+    def gemm(self, A, B, ta=False, tb=False, bias=None, out=None, colsum_b=None):
         a = A.T if ta else A
         b = B.T if tb else B
-        out = a @ b
-        return out if bias is None else out + bias
+        r = a @ b
+        if bias is not None:
+            r = r + bias
+        if colsum_b is not None:
+            colsum_b.copy_(B.sum(0))
+        if out is None:
+            return r
+        out.copy_(r)
+        return out
 
     def colsum(self, X):
         return X.sum(0)
