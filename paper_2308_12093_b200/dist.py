@@ -243,3 +243,47 @@ class DistGcnLayer:
                 ops.gemm(G_local, theta, tb=True, out=mine)
                 d_input = ops.spmm(self.AT, self._exchange(buf))
         return d_theta, d_bias, d_input
+
+    def step_host(self, hX, theta, bias, scheme, hG, needs_feature_grad, h_out, h_d_theta,
+                  h_d_bias, h_d_input=None, static_input=False):
+        """Forward + backward of this rank's row block from HOST buffers
+        (pinned), the counterpart of sgnn_gcn_step_host: X / dX' blocks are
+        copied in and out / grads copied out on side streams, overlapped with
+        compute and with each other.  Stream-ordered on the current stream."""
+        cs = torch.cuda.current_stream()
+        if not hasattr(self, "_s_in"):
+            self._s_in, self._s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        s_in, s_out = self._s_in, self._s_out
+        s_in.wait_stream(cs)
+        s_out.wait_stream(cs)
+        dev = cs.device
+        with torch.cuda.stream(s_in):
+            X = hX.to(dev, non_blocking=True)
+            ev_x = torch.cuda.Event()
+            ev_x.record(s_in)
+            G = hG.to(dev, non_blocking=True)
+            ev_g = torch.cuda.Event()
+            ev_g.record(s_in)
+        X.record_stream(cs)
+        G.record_stream(cs)
+        cs.wait_event(ev_x)
+        out, cache = self.forward(X, theta, bias, scheme, static_input=static_input)
+        ev_o = torch.cuda.Event()
+        ev_o.record(cs)
+        s_out.wait_event(ev_o)
+        with torch.cuda.stream(s_out):
+            h_out.copy_(out, non_blocking=True)
+        out.record_stream(s_out)
+        cs.wait_event(ev_g)
+        d_theta, d_bias, d_input = self.backward(G, theta, cache, needs_feature_grad)
+        ev_b = torch.cuda.Event()
+        ev_b.record(cs)
+        s_out.wait_event(ev_b)
+        with torch.cuda.stream(s_out):
+            h_d_theta.copy_(d_theta, non_blocking=True)
+            h_d_bias.copy_(d_bias, non_blocking=True)
+            if needs_feature_grad:
+                h_d_input.copy_(d_input, non_blocking=True)
+        for t in (d_theta, d_bias) + ((d_input,) if needs_feature_grad else ()):
+            t.record_stream(s_out)
+        cs.wait_stream(s_out)

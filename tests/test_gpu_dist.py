@@ -82,3 +82,24 @@ def test_partition_blocks_bit_identical(orc, parts):
         tb = pd.transposed_block(op.rows, op.cols, op.vals.astype(np.float32), r0, r1)
         AT_p = ops.adjacency(r1 - r0, n, *tb, torch.float32)
         assert torch.equal(AT_p.spmm(B), refT[r0:r1])
+
+
+def test_dist_step_host_matches_device_path(nccl_world1, orc):
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m, k = 2500, 32, 24
+    _, s, t = orc.synthetic_graph(n, 8.0, 2)
+    op = orc.gcn_operator(n, s, t)
+    layer = pd.DistGcnLayer(n, op.rows, op.cols, op.vals, pd.DeviceOps("cuda:0"), torch.float32)
+    X = torch.rand(n, m) * 2 - 1
+    G = torch.rand(n, k) * 2 - 1
+    th, bi = (torch.from_numpy(a.astype(np.float32)).cuda() for a in orc.gcn_params(m, k, 13))
+    for scheme in [(0, 0, 0), (2, 2, 1), (1, 1, 0)]:
+        out, cache = layer.forward(X.cuda(), th, bi, scheme)
+        ref = (out,) + layer.backward(G.cuda(), th, cache, True)
+        pin = lambda *sh: torch.empty(sh).pin_memory()  # noqa: E731
+        hs = (pin(n, k), pin(m, k), pin(k), pin(n, m))
+        layer.step_host(X.pin_memory(), th, bi, scheme, G.pin_memory(), True, *hs)
+        torch.cuda.synchronize()
+        for a, b in zip(hs, ref):
+            assert torch.equal(a, b.cpu()), scheme
