@@ -463,6 +463,25 @@ def run_ours_dist(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     mean_ms = float(t.item())
 
+    # 2-layer GCN training step (config 4 shape) over the same partition
+    model = pd.DistGcn2(layer, M_IN, GCN2_HID, MODEL_OUT, SEED + 13, caching=True)
+    tgt = d.random_uniform(ARXIV_N, MODEL_OUT, SEED + 12, ctx=ctx)[r0:r1].contiguous()
+    for _ in range(2):
+        model.train_step(X, tgt)
+    torch.cuda.synchronize()
+    mms = []
+    for _ in range(max(3, args.steps)):
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        model.train_step(X, tgt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        mms.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(mms) / len(mms)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    gcn2_ms = float(t.item())
+
     # e2e: each rank's row block of X and dX' from pinned host memory, the
     # rank's rows of out / dX and (rank 0) dTheta / db back to the host
     hX, hG = X.cpu().pin_memory(), G.cpu().pin_memory()
@@ -504,6 +523,8 @@ def run_ours_dist(args):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": None, "cpu_baseline": None,
+            "models": {"gcn2": {"ms": round(gcn2_ms, 4),
+                                "shape": f"{M_IN}-{GCN2_HID}-{MODEL_OUT}", "caching": True}},
             "edges_per_s": round(int(r.numel()) / (mean_ms * 1e-3), 1),
             "rows_per_rank": [layer.bounds[p + 1] - layer.bounds[p] for p in range(world)],
         }

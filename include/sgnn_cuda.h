@@ -264,6 +264,19 @@ typedef struct {
   int32_t input_grad;    /* compute d(input features) */
 } sgnn_model_config;
 typedef struct sgnn_model_s* sgnn_model;
+/* activation (dense.hpp:197-228): kind 0 relu, 2 elu(alpha = 1); out may
+ * alias x; mask[i] = x[i] > 0 (count bytes) */
+int sgnn_activation(sgnn_ctx ctx, int kind, int dtype, const void* x, int64_t count, void* out,
+                    uint8_t* mask);
+/* activation_backward (dense.hpp:232-268): elu needs the saved forward output */
+int sgnn_activation_backward(sgnn_ctx ctx, int kind, int dtype, const void* grad_out,
+                             const uint8_t* mask, const void* saved, int64_t count,
+                             void* grad_in);
+/* loss_mse (model.hpp): grad = 2 (out - target) / total, *loss (DEVICE double)
+ * = sum (out - target)^2 / total over the count elements given; total is the
+ * size of the whole prediction (== count unless the caller holds a block) */
+int sgnn_loss_mse(sgnn_ctx ctx, int dtype, const void* out, const void* target, int64_t count,
+                  int64_t total, void* grad, double* loss);
 int sgnn_model_create(sgnn_ctx ctx, const sgnn_model_config* cfg, uint64_t seed, int dtype,
                       sgnn_model* out);
 int sgnn_model_destroy(sgnn_model model);

@@ -106,6 +106,9 @@ _SIGS = {
     "sgnn_gat_cache_edge_values": (INT, [VP, VP, VP, VP, VP, VP, VP, VP]),
     "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
                                  VP, VP]),
+    "sgnn_activation": (INT, [VP, INT, INT, VP, I64, VP, VP]),
+    "sgnn_activation_backward": (INT, [VP, INT, INT, VP, VP, VP, I64, VP]),
+    "sgnn_loss_mse": (INT, [VP, INT, VP, VP, I64, I64, VP, VP]),
     "sgnn_model_create": (INT, [VP, C.POINTER(ModelConfig), U64, INT, PVP]),
     "sgnn_model_destroy": (INT, [VP]),
     "sgnn_model_num_params": (INT, [VP, PI32]),

@@ -98,11 +98,14 @@ void act_bwd(sgnn_ctx ctx, int kind, int64_t n, const T* g, const uint8_t* mask,
                                                                 out);
   launched(ctx);
 }
+// total: the element count of the whole prediction (row-partitioned callers
+// hold a block of it); the loss written is the block's sum of squares / total
 template <class T>
-void mse(sgnn_ctx ctx, int64_t n, const T* out, const T* target, T* grad, double* loss) {
-  const int nb = grid_for(ctx, n, 256);
+void mse(sgnn_ctx ctx, int64_t n, const T* out, const T* target, T* grad, double* loss,
+         int64_t total = 0) {
+  const int nb = grid_for(ctx, n > 0 ? n : 1, 256);
   DevBuf part((size_t)nb * sizeof(double), ctx->stream);
-  const double inv = 1.0 / (double)n;
+  const double inv = 1.0 / (double)(total > 0 ? total : n);
   k_mse<T><<<nb, 256, 0, ctx->stream>>>(n, out, target, inv, grad, part.as<double>());
   launched(ctx);
   k_mse_final<<<1, 256, 0, ctx->stream>>>(nb, part.as<double>(), inv, loss);
@@ -253,6 +256,47 @@ int sgnn_model_create(sgnn_ctx ctx, const sgnn_model_config* cfg, uint64_t seed,
     throw;
   }
   *out = md;
+  SGNN_API_END
+}
+
+int sgnn_activation(sgnn_ctx ctx, int kind, int dtype, const void* x, int64_t count, void* out,
+                    uint8_t* mask) {
+  SGNN_API_BEGIN
+  require(kind == 0 || kind == 2, "activation: relu (0) or elu (2)");
+  if (count == 0) return SGNN_OK;
+  if (dtype == SGNN_F32)
+    act_fwd<float>(ctx, kind, count, (const float*)x, (float*)out, mask);
+  else
+    act_fwd<double>(ctx, kind, count, (const double*)x, (double*)out, mask);
+  SGNN_API_END
+}
+
+int sgnn_activation_backward(sgnn_ctx ctx, int kind, int dtype, const void* grad_out,
+                             const uint8_t* mask, const void* saved, int64_t count,
+                             void* grad_in) {
+  SGNN_API_BEGIN
+  require(kind == 0 || kind == 2, "activation: relu (0) or elu (2)");
+  require(kind != 2 || saved != nullptr,
+          "activation_backward: elu requires the saved forward output");
+  if (count == 0) return SGNN_OK;
+  if (dtype == SGNN_F32)
+    act_bwd<float>(ctx, kind, count, (const float*)grad_out, mask, (const float*)saved,
+                   (float*)grad_in);
+  else
+    act_bwd<double>(ctx, kind, count, (const double*)grad_out, mask, (const double*)saved,
+                    (double*)grad_in);
+  SGNN_API_END
+}
+
+int sgnn_loss_mse(sgnn_ctx ctx, int dtype, const void* out, const void* target, int64_t count,
+                  int64_t total, void* grad, double* loss) {
+  SGNN_API_BEGIN
+  require(count >= 0 && total >= count && total > 0, "loss_mse: target shape mismatch");
+  if (dtype == SGNN_F32)
+    mse<float>(ctx, count, (const float*)out, (const float*)target, (float*)grad, loss, total);
+  else
+    mse<double>(ctx, count, (const double*)out, (const double*)target, (double*)grad, loss,
+                total);
   SGNN_API_END
 }
 

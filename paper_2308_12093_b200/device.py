@@ -536,6 +536,44 @@ def gat_backward(pattern: Pattern, d_out, theta, a_src, a_dst, cache: GatCache,
     return d_theta, d_as, d_ad, d_b, d_x
 
 
+# ---- activations / loss (dense.hpp:197-268, model.hpp loss_mse) ---------------
+_ACT = {"relu": 0, "elu": 2}
+
+
+def activation(X, kind, out=None, ctx=None):
+    """(out, mask): relu or elu(1); out may be X itself (in place)."""
+    ctx = _ctx(ctx)
+    X = X.contiguous()
+    out = torch.empty_like(X) if out is None else out
+    mask = torch.empty(X.shape, dtype=torch.uint8, device=X.device)
+    check(lib.sgnn_activation(ctx.handle, _ACT[kind], _dt(X), _p(X), X.numel(), _p(out),
+                              _p(mask)))
+    return out, mask
+
+
+def activation_backward(grad_out, mask, kind, saved=None, out=None, ctx=None):
+    ctx = _ctx(ctx)
+    grad_out = grad_out.contiguous()
+    out = torch.empty_like(grad_out) if out is None else out
+    check(lib.sgnn_activation_backward(ctx.handle, _ACT[kind], _dt(grad_out), _p(grad_out),
+                                       _p(mask), _p(saved), grad_out.numel(), _p(out)))
+    return out
+
+
+def loss_mse(out, target, total=None, ctx=None):
+    """(loss device float64 scalar, grad); total = size of the whole
+    prediction when `out` is a row block of it."""
+    ctx = _ctx(ctx)
+    out, target = out.contiguous(), target.contiguous()
+    if out.shape != target.shape:
+        raise ValueError("loss_mse: target shape mismatch")
+    grad = torch.empty_like(out)
+    loss = torch.zeros((), dtype=torch.float64, device=out.device)
+    check(lib.sgnn_loss_mse(ctx.handle, _dt(out), _p(out), _p(target), out.numel(),
+                            out.numel() if total is None else int(total), _p(grad), _p(loss)))
+    return loss, grad
+
+
 # ---- two-layer models (model.hpp:16-245) -----------------------------------------
 class Model:
     """Gcn2Model / Gat2Model (model.hpp:40-245) over sgnn_model: GCN -> ReLU ->

@@ -287,3 +287,39 @@ class DistGcnLayer:
         for t in (d_theta, d_bias) + ((d_input,) if needs_feature_grad else ()):
             t.record_stream(s_out)
         cs.wait_stream(s_out)
+
+
+class DistGcn2:
+    """Gcn2Model (model.hpp:40-115: GCN -> ReLU -> GCN, MSE step) over the
+    row partition: both layers share the rank's operator blocks; the hidden
+    activation, the loss and its gradient are computed on the rank's rows
+    (the loss sum is all-reduced, the gradient normalised by the global
+    size); parameter gradients are all-reduced inside the layers.  Parameters
+    are replicated, initialised like the reference (seed, seed + 101)."""
+
+    def __init__(self, layer: DistGcnLayer, m, hidden, out, seed, policy="adaptive",
+                 caching=True, input_grad=False, dtype=torch.float32):
+        from . import device as d
+
+        self.d, self.layer = d, layer
+        self.p = list(d.gcn_params(m, hidden, seed, dtype=dtype)) + \
+            list(d.gcn_params(hidden, out, seed + 101, dtype=dtype))
+        s1 = d.resolve_scheme(policy, m, hidden, input_grad, caching)
+        s2 = d.resolve_scheme(policy, hidden, out, True, caching)  # model.hpp:61-62
+        self.s1 = (s1.forward, s1.backward, s1.caching)
+        self.s2 = (s2.forward, s2.backward, s2.caching)
+        self.input_grad, self.out = input_grad, out
+
+    def train_step(self, X_local, target_local, static_input=True):
+        d, L = self.d, self.layer
+        th1, b1, th2, b2 = self.p
+        h, c1 = L.forward(X_local, th1, b1, self.s1, static_input=static_input)
+        h, mask = d.activation(h, "relu", out=h)
+        o, c2 = L.forward(h, th2, b2, self.s2)
+        loss, g = d.loss_mse(o, target_local, total=L.n * self.out)
+        if L.world > 1:
+            dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=L.group)
+        dth2, db2, dh = L.backward(g, th2, c2, True)
+        dh = d.activation_backward(dh, mask, "relu", out=dh)
+        dth1, db1, dx = L.backward(dh, th1, c1, self.input_grad)
+        return loss, o, [dth1, db1, dth2, db2], dx

@@ -103,3 +103,45 @@ def test_dist_step_host_matches_device_path(nccl_world1, orc):
         torch.cuda.synchronize()
         for a, b in zip(hs, ref):
             assert torch.equal(a, b.cpu()), scheme
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-10), (torch.float32, 1e-4)])
+def test_dist_gcn2_matches_oracle_model(nccl_world1, orc, dtype, tol):
+    """Partitioned 2-layer GCN step (world 1) against oracle.gcn2_step, which is
+    pinned to the reference's Gcn2Model step."""
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m, hid, o, seed = 1500, 20, 16, 6, 4
+    _, s, t = orc.synthetic_graph(n, 7.0, 3)
+    op = orc.gcn_operator(n, s, t)
+    layer = pd.DistGcnLayer(n, op.rows, op.cols, op.vals, pd.DeviceOps("cuda:0"), dtype)
+    model = pd.DistGcn2(layer, m, hid, o, seed, caching=True, input_grad=False, dtype=dtype)
+    X = orc.random_uniform(n, m, seed + 11)
+    target = orc.random_uniform(n, o, seed + 12)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)  # noqa: E731
+    loss, out, grads, _ = model.train_step(cu(X), cu(target))
+    rl, rout, rgrads, _ = orc.gcn2_step(op, X, orc.gcn2_params(m, hid, o, seed), target, 0, True,
+                                        False)
+    assert abs(float(loss) - rl) <= tol * max(1.0, abs(rl))
+    assert orc.max_rel_diff(out.double().cpu().numpy(), rout) < tol
+    for g, r in zip(grads, rgrads):
+        assert orc.max_rel_diff(g.double().cpu().numpy(), r) < tol
+
+
+def test_activation_and_loss_entry_points(orc):
+    from paper_2308_12093_b200 import device as d
+
+    x = torch.randn(1000, 7, dtype=torch.float64, device="cuda")
+    for kind, prm in (("relu", 0.0), ("elu", 1.0)):
+        h, mask = d.activation(x, kind)
+        rh, rmask = orc.activation(x.cpu().numpy(), kind, prm)
+        assert orc.max_rel_diff(h.cpu().numpy(), rh) < 1e-15
+        assert np.array_equal(mask.cpu().numpy(), rmask)
+        g = torch.randn_like(x)
+        gi = d.activation_backward(g, mask, kind, saved=h)
+        rgi = orc.activation_backward(g.cpu().numpy(), rmask, kind, prm, rh)
+        assert orc.max_rel_diff(gi.cpu().numpy(), rgi) < 1e-15
+    tgt = torch.randn_like(x)
+    loss, grad = d.loss_mse(x, tgt)
+    rl, rg = orc.loss_mse(x.cpu().numpy(), tgt.cpu().numpy())
+    assert abs(float(loss) - rl) < 1e-12 and orc.max_rel_diff(grad.cpu().numpy(), rg) < 1e-15
