@@ -371,6 +371,17 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
       else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f);
       return;
     }
+    if (mode == 0 && vec_ok && f > 256) {
+      // wide rows: 256-column windows through the lean kernel (row stride f);
+      // one thread still accumulates each output element in stored edge order
+      for (int32_t c0 = 0; c0 < f; c0 += 256) {
+        const int32_t w = f - c0 < 256 ? f - c0 : 256;
+        const float* bw = bias ? bias + c0 : nullptr;
+        if (w <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f);
+        else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f);
+      }
+      return;
+    }
   }
   if (f % VW == 0 && aligned)
     launch_w<T, VW>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f);
