@@ -463,6 +463,36 @@ def run_ours_dist(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     mean_ms = float(t.item())
 
+    # GAT layer (h=8, k=32) over the same row partition of the GAT pattern
+    Pg = d.Pattern.gat_pattern(ARXIV_N, src, dst, ctx)
+    pa = Pg.arrays()
+    rp_h, cl_h = pa["rowptr"].cpu().numpy(), pa["cols"].cpu().numpy()
+    glayer = pd.DistGatLayer(ARXIV_N, rp_h, cl_h, GAT_H, GAT_K, dev)
+    g0, g1 = glayer.r0, glayer.r1
+    th_g, as_g, ad_g, b_g = d.gat_params(M_IN, GAT_H, GAT_K, SEED + 13, ctx=ctx)
+    Xg = d.random_uniform(ARXIV_N, M_IN, SEED + 11, ctx=ctx)[g0:g1].contiguous()
+    Gg = d.random_uniform(ARXIV_N, GAT_H * GAT_K, SEED + 12, ctx=ctx)[g0:g1].contiguous()
+
+    def gat_step():
+        o, c = glayer.forward(Xg, th_g, as_g, ad_g, b_g)
+        return glayer.backward(Gg, th_g, as_g, ad_g, c, True)
+
+    for _ in range(2):
+        gat_step()
+    torch.cuda.synchronize()
+    gms = []
+    for _ in range(max(3, args.steps)):
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gat_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gms.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(gms) / len(gms)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    gat_ms = float(t.item())
+
     # 2-layer GCN training step (config 4 shape) over the same partition
     model = pd.DistGcn2(layer, M_IN, GCN2_HID, MODEL_OUT, SEED + 13, caching=True)
     tgt = d.random_uniform(ARXIV_N, MODEL_OUT, SEED + 12, ctx=ctx)[r0:r1].contiguous()
@@ -523,6 +553,9 @@ def run_ours_dist(args):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": None, "cpu_baseline": None,
+            "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K,
+                          "partition": "row blocks of the GAT pattern (all-gather M, d, dX', "
+                                       "alpha, dy)"},
             "models": {"gcn2": {"ms": round(gcn2_ms, 4),
                                 "shape": f"{M_IN}-{GCN2_HID}-{MODEL_OUT}", "caching": True}},
             "edges_per_s": round(int(r.numel()) / (mean_ms * 1e-3), 1),

@@ -106,6 +106,14 @@ _SIGS = {
     "sgnn_gat_cache_edge_values": (INT, [VP, VP, VP, VP, VP, VP, VP, VP]),
     "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
                                  VP, VP]),
+    "sgnn_gat_transform": (INT, [VP, VP, I32, I32, VP, I32, I32, VP, VP, VP, VP, VP]),
+    "sgnn_gat_attention": (INT, [VP, I32, VP, VP, I32, VP, VP, D, VP, VP]),
+    "sgnn_gat_aggregate": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP]),
+    "sgnn_gat_sddmm": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP]),
+    "sgnn_gat_softmax_backward": (INT, [VP, I32, VP, I32, VP, VP, VP, D, VP, VP]),
+    "sgnn_gat_column_pass": (INT, [VP, I32, VP, VP, VP, I32, I32, VP, VP, VP, VP, VP, VP, VP,
+                                   VP]),
+    "sgnn_gat_param_grads": (INT, [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP]),
     "sgnn_activation": (INT, [VP, INT, INT, VP, I64, VP, VP]),
     "sgnn_activation_backward": (INT, [VP, INT, INT, VP, VP, VP, I64, VP]),
     "sgnn_loss_mse": (INT, [VP, INT, VP, VP, I64, I64, VP, VP]),

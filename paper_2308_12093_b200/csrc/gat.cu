@@ -1099,4 +1099,151 @@ int sgnn_sddmm(sgnn_ctx ctx, sgnn_pattern p, const void* B, int32_t f, const voi
   SGNN_API_END
 }
 
+
+// ---------------------------------------------------------------------------
+// Kernel-level GAT pieces over row / column blocks (float32, the v2 shapes:
+// h in {1,2,4,8}, k % 4 == 0, h*k <= 1024).  They are the reference's kernel
+// functions (kernels.hpp) as separate calls so a row-partitioned layer can
+// interleave them with NCCL exchanges: column ids index a (gathered) operand
+// of any row count, row ids are block-local.  All pointers 16-byte aligned.
+// ---------------------------------------------------------------------------
+static void block_check(int32_t h, int32_t k) {
+  require(v2_R<float>(h, k) != 0, "gat block: needs h in {1,2,4,8}, k % 4 == 0, h*k <= 1024");
+}
+
+// node_scores (kernels.hpp:385-423) fused into M = X Theta when k % 32 == 0
+int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
+                       const float* theta, int32_t h, int32_t k, const float* a_src,
+                       const float* a_dst, float* M, float* s, float* d) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  if (n_rows == 0) return SGNN_OK;
+  if (!gemm_scores_f32(ctx, X, n_rows, m, theta, h * k, M, a_src, a_dst, h, s, d)) {
+    gemm<float>(ctx, X, n_rows, m, theta, m, h * k, false, false, M);
+    const int R = fast_R<float>(h, k);
+    if (R) node_scores_fast<float>(ctx, R, n_rows, h, k, M, a_src, a_dst, s, d);
+    else node_scores<float>(ctx, n_rows, h, k, M, a_src, a_dst, s, d);
+  }
+  SGNN_API_END
+}
+
+// edge_scores + leaky_relu_edges + edge_softmax (kernels.hpp:427-534):
+// alpha, mask edge-major (q_local x h) for the block's rows; s block-local,
+// d indexed by column id
+int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
+                       const int32_t* cols, int32_t h, const float* s, const float* d,
+                       double beta, float* alpha, uint8_t* mask) {
+  SGNN_API_BEGIN
+  require(beta > 0, "gat_forward: beta must be positive");
+  require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
+  if (n_rows == 0) return SGNN_OK;
+  HR_SWITCH(h, 1, (g2::k_gat_attn4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
+                      n_rows, rowptr, cols, s, d, (float)beta, alpha, mask)));
+  launched(ctx);
+  SGNN_API_END
+}
+
+// spmm_semibatched + bias (kernels.hpp:219-254): out rows of the block
+int sgnn_gat_aggregate(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
+                       int32_t h, int32_t k, const float* alpha, const float* M,
+                       const float* bias, float* out) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  if (n_rows == 0) return SGNN_OK;
+  const int R2 = v2_R<float>(h, k);
+  HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+                       n_rows, rowptr, cols, alpha, reinterpret_cast<const float4*>(M), k,
+                       reinterpret_cast<const float4*>(bias), reinterpret_cast<float4*>(out))));
+  launched(ctx);
+  SGNN_API_END
+}
+
+// sddmm_semibatched (kernels.hpp:342-377): dAlpha edge-major for the block's rows
+int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
+                   int32_t h, int32_t k, const float* M, const float* G, float* da) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  if (n_rows == 0) return SGNN_OK;
+  const int R2 = v2_R<float>(h, k);
+  const int L = k / 4;
+  const float4* M4 = reinterpret_cast<const float4*>(M);
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  if ((L & (L - 1)) == 0 && L <= 32) {
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+                         n_rows, rowptr, cols, M4, G4, k, da)));
+  } else {
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+                         n_rows, rowptr, cols, M4, G4, k, da)));
+  }
+  launched(ctx);
+  SGNN_API_END
+}
+
+// edge_softmax_backward + leaky_relu_edges_backward + edge_row_sums
+// (kernels.hpp:481-495, 537-588)
+int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
+                              const float* alpha, const uint8_t* mask, const float* da,
+                              double beta, float* dy, float* dS) {
+  SGNN_API_BEGIN
+  require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
+  if (n_rows == 0) return SGNN_OK;
+  HR_SWITCH(h, 1, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
+                      n_rows, rowptr, alpha, mask, da, (float)beta, dy, dS)));
+  launched(ctx);
+  SGNN_API_END
+}
+
+// spmm_semibatched_transposed + edge_col_sums + add_scaled_rows_inplace
+// (kernels.hpp:258-295, 614-658) over a block of columns: colptr / rows /
+// perm of the block (rows and perm index the gathered G and alpha / dy)
+int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
+                         const int32_t* rows, const int32_t* perm, int32_t h, int32_t k,
+                         const float* G, const float* alpha, const float* dy, const float* dS,
+                         const float* a_src, const float* a_dst, float* dD, float* dM) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  if (n_cols == 0) return SGNN_OK;
+  const int R2 = v2_R<float>(h, k);
+  HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<v2_grid(n_cols), 256, 0, ctx->stream>>>(
+                       n_cols, colptr, rows, perm, reinterpret_cast<const float4*>(G), alpha, dy,
+                       dS, reinterpret_cast<const float4*>(a_src),
+                       reinterpret_cast<const float4*>(a_dst), k, dD,
+                       reinterpret_cast<float4*>(dM))));
+  launched(ctx);
+  SGNN_API_END
+}
+
+// column_sums (d_bias) + attention_param_grad for a_src / a_dst
+// (dense.hpp:272-282, kernels.hpp:592-611) over the block's rows
+int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, const float* G,
+                         const float* M, const float* dS, const float* dD, float* d_bias,
+                         float* d_a_src, float* d_a_dst) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  const int32_t hk = h * k;
+  if (n_rows == 0) {
+    SGNN_CUDA(cudaMemsetAsync(d_bias, 0, hk * 4, ctx->stream));
+    SGNN_CUDA(cudaMemsetAsync(d_a_src, 0, hk * 4, ctx->stream));
+    SGNN_CUDA(cudaMemsetAsync(d_a_dst, 0, hk * 4, ctx->stream));
+    return SGNN_OK;
+  }
+  cudaStream_t st = ctx->stream;
+  const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(2 * ctx->num_sms, n_rows));
+  const int32_t chunk = (int32_t)ceil_div(n_rows, nb);
+  DevBuf part((size_t)nb * 3 * hk * sizeof(double), st);
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  const float4* M4 = reinterpret_cast<const float4*>(M);
+  switch (h) {
+    case 1: g2::k_grads3_partial<1><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    case 2: g2::k_grads3_partial<2><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    case 4: g2::k_grads3_partial<4><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    default: g2::k_grads3_partial<8><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+  }
+  launched(ctx);
+  g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(
+      nb, hk, part.as<double>(), d_bias, d_a_src, d_a_dst);
+  launched(ctx);
+  SGNN_API_END
+}
+
 }  // extern "C"

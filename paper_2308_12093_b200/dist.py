@@ -323,3 +323,148 @@ class DistGcn2:
         dh = d.activation_backward(dh, mask, "relu", out=dh)
         dth1, db1, dx = L.backward(dh, th1, c1, self.input_grad)
         return loss, o, [dth1, db1, dth2, db2], dx
+
+
+# ---------------------------------------------------------------------------
+# partitioned GAT layer (gat.hpp:89-219 over row blocks)
+# ---------------------------------------------------------------------------
+def gat_blocks(rowptr, cols, bounds, rank):
+    """Host-side index arrays of rank's blocks of a GAT pattern (CSR with all
+    self loops, canonical order).  Row block: local rowptr and the columns
+    remapped to the padded node layout.  Column block (columns [r0, r1), i.e.
+    rows of A^T, rows ascending within a column like the reference's CSC,
+    sparse.hpp:207-216): local colptr, the rows remapped to the padded node
+    layout, and perm = the padded edge index of each entry -- the edges of
+    rank p's rows occupy slot p (emx entries) of a gathered edge-major array."""
+    rowptr = np.asarray(rowptr, np.int64)
+    cols = np.asarray(cols, np.int64)
+    world = len(bounds) - 1
+    mx = max(bounds[p + 1] - bounds[p] for p in range(world))
+    ebounds = [int(rowptr[b]) for b in bounds]
+    emx = max(ebounds[p + 1] - ebounds[p] for p in range(world))
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    e0, e1 = ebounds[rank], ebounds[rank + 1]
+    rp = (rowptr[r0:r1 + 1] - e0).astype(np.int32)
+    cl = padded_columns(cols[e0:e1], bounds, mx)
+    n = len(rowptr) - 1
+    rows_of = np.repeat(np.arange(n, dtype=np.int64), np.diff(rowptr))
+    sel = np.nonzero((cols >= r0) & (cols < r1))[0]  # canonical edge ids, row-major
+    lc = cols[sel] - r0
+    order = np.argsort(lc, kind="stable")  # rows stay ascending within a column
+    e = sel[order]
+    r = rows_of[e]
+    colptr = np.zeros(r1 - r0 + 1, np.int64)
+    np.add.at(colptr, lc[order] + 1, 1)
+    colptr = np.cumsum(colptr).astype(np.int32)
+    owner = np.searchsorted(np.asarray(bounds, np.int64), r, side="right") - 1
+    perm = (owner * emx + (e - np.asarray(ebounds, np.int64)[owner])).astype(np.int32)
+    return {"rowptr": rp, "cols": cl, "colptr": colptr,
+            "rows": padded_columns(r, bounds, mx), "perm": perm, "mx": mx, "emx": emx,
+            "edges": e1 - e0}
+
+
+class DistGatLayer:
+    """One GAT layer (float32, h in {1,2,4,8}, k % 4 == 0) over the row
+    partition.  Forward: M = X_p Theta with the node scores (own rows) into
+    the rank's slots of the padded M / d gather buffers, all-gather, then
+    attention and aggregation of the rank's rows.  Backward: SDDMM and the
+    softmax backward on the rank's rows, all-gather of dX', alpha and dy
+    (edge-major; each rank's edges are one contiguous slot), the column pass
+    over the rank's columns (rows of A^T), parameter gradients on the rank's
+    rows, one packed all-reduce.  Every piece is a libsgnn_cuda.so kernel
+    (the sgnn_gat_* block entry points)."""
+
+    def __init__(self, n, rowptr, cols, heads, k, device, group=None):
+        from . import _capi
+        from .device import Context
+
+        self.c = _capi
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n, self.h, self.k = n, heads, k
+        self.dev = torch.device(device)
+        self.bounds = partition_rows(rowptr, self.world)
+        self.r0, self.r1 = self.bounds[self.rank], self.bounds[self.rank + 1]
+        b = gat_blocks(rowptr, cols, self.bounds, self.rank)
+        self.mx, self.emx, self.ne = b["mx"], b["emx"], b["edges"]
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.dev)  # noqa: E731
+        self.rowptr, self.cols = t(b["rowptr"]), t(b["cols"])
+        self.colptr, self.crows, self.perm = t(b["colptr"]), t(b["rows"]), t(b["perm"])
+        self.ctx = Context.default(self.dev.index)
+
+    def _buf(self, slots, width, used, dtype=torch.float32):
+        buf = torch.empty((self.world * slots, width), dtype=dtype, device=self.dev)
+        lo = self.rank * slots
+        return buf, buf[lo: lo + used]
+
+    def _exchange(self, buf, slots):
+        if self.world > 1:
+            lo = self.rank * slots
+            dist.all_gather_into_tensor(buf, buf[lo: lo + slots], group=self.group)
+        return buf
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else t.data_ptr()
+
+    def forward(self, X_local, theta, a_src, a_dst, bias, beta=0.2):
+        c, lib, P = self.c, self.c.lib, self._p
+        h, k, nl = self.h, self.k, self.r1 - self.r0
+        X_local = X_local.contiguous()
+        Mbuf, Mmine = self._buf(self.mx, h * k, nl)
+        dbuf, dmine = self._buf(self.mx, h, nl)
+        s_loc = torch.empty((nl, h), dtype=torch.float32, device=self.dev)
+        c.check(lib.sgnn_gat_transform(self.ctx.handle, P(X_local), nl, X_local.shape[1],
+                                       P(theta), h, k, P(a_src), P(a_dst), P(Mmine), P(s_loc),
+                                       P(dmine)))
+        self._exchange(Mbuf, self.mx)
+        self._exchange(dbuf, self.mx)
+        abuf, amine = self._buf(self.emx, h, self.ne)
+        mask = torch.empty((self.ne, h), dtype=torch.uint8, device=self.dev)
+        c.check(lib.sgnn_gat_attention(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h,
+                                       P(s_loc), P(dbuf), float(beta), P(amine), P(mask)))
+        out = torch.empty((nl, h * k), dtype=torch.float32, device=self.dev)
+        c.check(lib.sgnn_gat_aggregate(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h, k,
+                                       P(amine), P(Mbuf), P(bias), P(out)))
+        return out, {"X": X_local, "M": Mbuf, "Mmine": Mmine, "alpha": abuf, "amine": amine,
+                     "mask": mask, "beta": beta}
+
+    def backward(self, G_local, theta, a_src, a_dst, cache, needs_feature_grad):
+        from . import device as d
+
+        c, lib, P = self.c, self.c.lib, self._p
+        h, k, nl = self.h, self.k, self.r1 - self.r0
+        hk = h * k
+        beta = cache["beta"]
+        Gbuf, Gmine = self._buf(self.mx, hk, nl)
+        Gmine.copy_(G_local)
+        da = torch.empty((self.ne, h), dtype=torch.float32, device=self.dev)
+        c.check(lib.sgnn_gat_sddmm(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h, k,
+                                   P(cache["M"]), P(Gmine), P(da)))
+        dybuf, dymine = self._buf(self.emx, h, self.ne)
+        dS = torch.empty((nl, h), dtype=torch.float32, device=self.dev)
+        c.check(lib.sgnn_gat_softmax_backward(self.ctx.handle, nl, P(self.rowptr), h,
+                                              P(cache["amine"]), P(cache["mask"]), P(da),
+                                              float(beta), P(dymine), P(dS)))
+        self._exchange(Gbuf, self.mx)
+        self._exchange(cache["alpha"], self.emx)
+        self._exchange(dybuf, self.emx)
+        dD = torch.empty((nl, h), dtype=torch.float32, device=self.dev)
+        dM = torch.empty((nl, hk), dtype=torch.float32, device=self.dev)
+        c.check(lib.sgnn_gat_column_pass(self.ctx.handle, nl, P(self.colptr), P(self.crows),
+                                         P(self.perm), h, k, P(Gbuf), P(cache["alpha"]),
+                                         P(dybuf), P(dS), P(a_src), P(a_dst), P(dD), P(dM)))
+        flat = torch.empty(theta.numel() + 3 * hk, dtype=torch.float32, device=self.dev)
+        d_theta = flat[:theta.numel()].view_as(theta)
+        d_b = flat[theta.numel():theta.numel() + hk]
+        d_as = flat[theta.numel() + hk:theta.numel() + 2 * hk].view(h, k)
+        d_ad = flat[theta.numel() + 2 * hk:].view(h, k)
+        c.check(lib.sgnn_gat_param_grads(self.ctx.handle, nl, h, k, P(Gmine),
+                                         P(cache["Mmine"]), P(dS), P(dD), P(d_b), P(d_as),
+                                         P(d_ad)))
+        d.gemm(cache["X"], dM, True, False, out=d_theta)
+        d_x = d.gemm(dM, theta, False, True) if needs_feature_grad else None
+        if self.world > 1:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        return d_theta, d_as, d_ad, d_b, d_x

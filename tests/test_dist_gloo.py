@@ -135,3 +135,37 @@ def test_partition_rows_balances_nnz():
     r, c, v = transposed_block(np.array([0, 0, 1, 2]), np.array([1, 2, 0, 1]),
                                np.array([1.0, 2.0, 3.0, 4.0]), 1, 3)
     assert list(r) == [0, 0, 1] and list(c) == [0, 2, 0] and list(v) == [1.0, 4.0, 2.0]
+
+
+def test_gat_blocks_reproduce_the_csc_view():
+    """Host index arrays of the partitioned GAT layer: over the ranks, the
+    column blocks are the pattern's CSC (rows ascending within a column) and
+    perm points at the right edges of the gathered edge-major layout."""
+    from paper_2308_12093_b200.dist import gat_blocks, partition_rows
+
+    rng = np.random.default_rng(3)
+    n = 300
+    A = (rng.random((n, n)) < 0.03) | np.eye(n, dtype=bool)
+    rows, cols = np.nonzero(A)
+    rowptr = np.concatenate([[0], np.cumsum(A.sum(1))])
+    for world in (1, 2, 3, 4):
+        bounds = partition_rows(rowptr, world)
+        mx = max(bounds[p + 1] - bounds[p] for p in range(world))
+        blocks = [gat_blocks(rowptr, cols, bounds, p) for p in range(world)]
+        emx = blocks[0]["emx"]
+        canon = {}
+        for p, b in enumerate(blocks):
+            for i in range(b["edges"]):
+                canon[p * emx + i] = rowptr[bounds[p]] + i
+        for p, b in enumerate(blocks):
+            r0 = bounds[p]
+            assert np.array_equal(b["rowptr"], rowptr[r0:bounds[p + 1] + 1] - rowptr[r0])
+            for jl in range(bounds[p + 1] - r0):
+                j = r0 + jl
+                lo, hi = b["colptr"][jl], b["colptr"][jl + 1]
+                want = list(np.nonzero(A[:, j])[0])
+                got = [bounds[q // mx] + q % mx for q in b["rows"][lo:hi]]
+                assert got == want
+                for q, r in zip(b["perm"][lo:hi], want):
+                    e = canon[int(q)]
+                    assert rows[e] == r and cols[e] == j

@@ -145,3 +145,32 @@ def test_activation_and_loss_entry_points(orc):
     loss, grad = d.loss_mse(x, tgt)
     rl, rg = orc.loss_mse(x.cpu().numpy(), tgt.cpu().numpy())
     assert abs(float(loss) - rl) < 1e-12 and orc.max_rel_diff(grad.cpu().numpy(), rg) < 1e-15
+
+
+@pytest.mark.parametrize("h,k", [(8, 32), (4, 12), (2, 64)])
+def test_dist_gat_layer_world1(nccl_world1, orc, h, k):
+    """Partitioned GAT layer (world 1): identical kernels in the same order as
+    the single-GPU layer (bit-identical results) and the oracle at 1e-4."""
+    from paper_2308_12093_b200 import device as d
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m = 2200, 24
+    _, s, t = orc.synthetic_graph(n, 8.0, 6)
+    pat = orc.gat_pattern(n, s, t)
+    layer = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, k, "cuda:0")
+    th, a_s, a_d, b = (torch.from_numpy(x.astype(np.float32)).cuda()
+                       for x in orc.gat_params(m, h, k, 21))
+    X = orc.random_uniform(n, m, 11)
+    G = orc.random_uniform(n, h * k, 12)
+    Xc = torch.from_numpy(X.astype(np.float32)).cuda()
+    Gc = torch.from_numpy(G.astype(np.float32)).cuda()
+    out, cache = layer.forward(Xc, th, a_s, a_d, b)
+    grads = layer.backward(Gc, th, a_s, a_d, cache, True)
+    P = d.Pattern(n, torch.from_numpy(pat.rowptr).cuda(), torch.from_numpy(pat.cols).cuda())
+    o1, c1 = d.gat_forward(P, Xc, th, a_s, a_d, b, h, 0.2, "full")
+    g1 = d.gat_backward(P, Gc, th, a_s, a_d, c1, True)
+    assert torch.equal(out, o1)
+    for a_, b_ in zip(grads, g1):
+        assert torch.equal(a_, b_)
+    ref_o = orc.gat_forward(pat, X, *orc.gat_params(m, h, k, 21), h, 0.2)
+    assert orc.max_rel_diff(out.double().cpu().numpy(), ref_o) < 1e-4
