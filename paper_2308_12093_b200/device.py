@@ -98,6 +98,38 @@ def _ctx(ctx):
     return ctx if ctx is not None else Context.default()
 
 
+class StepGraph:
+    """A stream-ordered step (layer or model calls without host
+    synchronisation) captured once into a CUDA graph and replayed: the same
+    kernels with the per-launch CPU overhead removed.  `fn` is warmed up,
+    captured on a side stream (the context's stream is switched for the
+    capture), and its return value -- tensors from the graph's memory pool,
+    rewritten by every replay -- is `outputs`."""
+
+    def __init__(self, fn, ctx=None, warmup=1):
+        self.ctx = ctx = _ctx(ctx)
+        dev = ctx.device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        prev = ctx.stream
+        ctx.set_stream(side)
+        try:
+            with torch.cuda.stream(side):
+                for _ in range(warmup):
+                    fn()
+                side.synchronize()
+                self.graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph, stream=side):
+                    self.outputs = fn()
+        finally:
+            ctx.set_stream(prev)
+        torch.cuda.current_stream(dev).wait_stream(side)
+
+    def replay(self):
+        self.graph.replay()
+        return self.outputs
+
+
 # ---- selector / model (host-pure) -----------------------------------------
 def resolve_scheme(policy, m, k, needs_feature_grad=False, caching=False) -> Scheme:
     """gcn.hpp:34-47; policy 'adaptive' | 'transform-first' | 'propagate-first'."""
