@@ -155,7 +155,18 @@ template void gemm_simt<double>(sgnn_ctx, const double*, int32_t, int32_t, const
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src = nullptr, const float* att_dst = nullptr,
-                 float* s_out = nullptr, float* d_out = nullptr, int heads = 0);
+                 float* s_out = nullptr, float* d_out = nullptr, int heads = 0,
+                 uint8_t* relu_out = nullptr, const uint8_t* mask_in = nullptr);
+
+// C = op(A) op(B) (+ bias) with ReLU fused into the epilogue: relu_out
+// receives the mask (forward), or mask_in zeroes C where the mask is 0
+// (backward).  false (nothing launched) when the shape does not allow it.
+bool gemm_relu_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                   int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
+                   uint8_t* relu_out, const uint8_t* mask_in) {
+  return gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, nullptr, nullptr, nullptr,
+                     nullptr, nullptr, 0, relu_out, mask_in);
+}
 
 // M = X Theta with the GAT node scores s, d (n x h) computed in the GEMM
 // epilogue; false when the fused form does not apply (nothing done)

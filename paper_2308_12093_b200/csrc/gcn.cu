@@ -15,9 +15,23 @@ using namespace sgnn;
 
 namespace {
 
+inline void ok(int rc) {
+  if (rc == SGNN_OK) return;
+  if (rc == SGNN_EINVAL) throw invalid_argument(sgnn_last_error());
+  throw std::runtime_error(sgnn_last_error());
+}
+
+template <class T>
+constexpr int dt() {
+  return sizeof(T) == 4 ? SGNN_F32 : SGNN_F64;
+}
+
+// out = A' X Theta + b, then (relu != nullptr) ReLU with its mask -- fused into
+// the X.Theta / P.Theta epilogue when that GEMM runs on tcgen05
 template <class T>
 void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* theta,
-                   const T* bias, int32_t k, const sgnn_scheme& s, T* out, sgnn_gcn_cache c) {
+                   const T* bias, int32_t k, const sgnn_scheme& s, T* out, sgnn_gcn_cache c,
+                   uint8_t* relu = nullptr) {
   const int32_t n = A->n_rows;
   cudaStream_t st = ctx->stream;
   const int32_t* rp = A->rowptr.as<int32_t>();
@@ -27,11 +41,19 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
     DevBuf M((size_t)n * k * sizeof(T), st);
     gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
     spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz);
+    if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
     c->saved_input = X;
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
     spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
-    gemm<T>(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias);
+    bool fused = false;
+    if constexpr (sizeof(T) == 4)
+      if (relu) fused = gemm_relu_f32(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias,
+                                      relu, nullptr);
+    if (!fused) {
+      gemm<T>(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias);
+      if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
+    }
     if (s.forward == SGNN_PROPAGATE_FIRST_CACHED)
       c->saved_propagated = std::move(P);  // reclassified into the cache (gcn.hpp:124)
     else
@@ -39,9 +61,17 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
   }
 }
 
+// d_input gets the ReLU backward of the previous layer applied when dmask is
+// given (fused into the S.Theta^T epilogue on the fused_propagate scheme)
 template <class T>
 void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_t m, int32_t k,
-                    sgnn_gcn_cache c, bool fg, T* d_theta, T* d_bias, T* d_input) {
+                    sgnn_gcn_cache c, bool fg, T* d_theta, T* d_bias, T* d_input,
+                    const uint8_t* dmask = nullptr) {
+  auto relu_bwd = [&]() {
+    if (dmask && fg)
+      ok(sgnn_activation_backward(ctx, 0, dt<T>(), d_input, dmask, nullptr,
+                                  (int64_t)A->n_cols * m, d_input));
+  };
   const int32_t n = A->n_rows;
   cudaStream_t st = ctx->stream;
   const int32_t* rp = A->rowptr.as<int32_t>();
@@ -57,7 +87,16 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       column_sums<T>(ctx, G, n, k, d_bias);
       spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz);
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
-      if (fg) gemm<T>(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input);
+      if (fg) {
+        bool fused = false;
+        if constexpr (sizeof(T) == 4)
+          if (dmask) fused = gemm_relu_f32(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input,
+                                           nullptr, nullptr, dmask);
+        if (!fused) {
+          gemm<T>(ctx, S.as<T>(), n, k, theta, m, k, false, true, d_input);
+          relu_bwd();
+        }
+      }
       break;
     }
     case SGNN_SPLIT_PROPAGATE: {
@@ -69,6 +108,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
         spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
+        relu_bwd();
       }
       break;
     }
@@ -79,6 +119,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
         spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
+        relu_bwd();
       }
       break;
     }
@@ -93,6 +134,22 @@ extern "C" {
 int sgnn_gcn_forward(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m, const void* theta,
                      const void* bias, int32_t k, const sgnn_scheme* scheme, void* out,
                      sgnn_gcn_cache* cache) {
+  return sgnn::gcn_forward_relu(ctx, A, X, m, theta, bias, k, scheme, out, cache, nullptr);
+}
+
+int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* theta, int32_t m,
+                      int32_t k, sgnn_gcn_cache c, int fg, void* d_theta, void* d_bias,
+                      void* d_input) {
+  return sgnn::gcn_backward_relu(ctx, A, d_out, theta, m, k, c, fg, d_theta, d_bias, d_input,
+                                 nullptr);
+}
+
+}  // extern "C"
+
+int sgnn::gcn_forward_relu(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m,
+                           const void* theta, const void* bias, int32_t k,
+                           const sgnn_scheme* scheme, void* out, sgnn_gcn_cache* cache,
+                           uint8_t* relu_mask) {
   SGNN_API_BEGIN
   require(A && scheme && cache, "gcn_forward: null argument");
   require(A->n_rows == A->n_cols, "gcn_forward: adjacency/input shape mismatch");
@@ -109,10 +166,10 @@ int sgnn_gcn_forward(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m, const v
   try {
     if (A->dtype == SGNN_F32)
       gcn_forward_t<float>(ctx, A, (const float*)X, m, (const float*)theta, (const float*)bias,
-                           k, *scheme, (float*)out, c);
+                           k, *scheme, (float*)out, c, relu_mask);
     else
       gcn_forward_t<double>(ctx, A, (const double*)X, m, (const double*)theta,
-                            (const double*)bias, k, *scheme, (double*)out, c);
+                            (const double*)bias, k, *scheme, (double*)out, c, relu_mask);
   } catch (...) {
     delete c;
     throw;
@@ -121,9 +178,9 @@ int sgnn_gcn_forward(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m, const v
   SGNN_API_END
 }
 
-int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* theta, int32_t m,
-                      int32_t k, sgnn_gcn_cache c, int fg, void* d_theta, void* d_bias,
-                      void* d_input) {
+int sgnn::gcn_backward_relu(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* theta,
+                            int32_t m, int32_t k, sgnn_gcn_cache c, int fg, void* d_theta,
+                            void* d_bias, void* d_input, const uint8_t* relu_mask_in) {
   SGNN_API_BEGIN
   require(c != nullptr, "gcn_backward: missing saved input");
   require(!c->consumed, "gcn_backward: cache already consumed");
@@ -138,14 +195,16 @@ int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* t
   require(!fg || d_input != nullptr, "gcn_backward: d_input required for feature gradients");
   if (A->dtype == SGNN_F32)
     gcn_backward_t<float>(ctx, A, (const float*)d_out, (const float*)theta, m, k, c, fg != 0,
-                          (float*)d_theta, (float*)d_bias, (float*)d_input);
+                          (float*)d_theta, (float*)d_bias, (float*)d_input, relu_mask_in);
   else
     gcn_backward_t<double>(ctx, A, (const double*)d_out, (const double*)theta, m, k, c, fg != 0,
-                           (double*)d_theta, (double*)d_bias, (double*)d_input);
+                           (double*)d_theta, (double*)d_bias, (double*)d_input, relu_mask_in);
   // the cached P is released once consumed (its lifetime ends with backward)
   c->saved_propagated.reset();
   SGNN_API_END
 }
+
+extern "C" {
 
 int sgnn_gcn_cache_destroy(sgnn_gcn_cache c) {
   SGNN_API_BEGIN

@@ -196,6 +196,11 @@ struct EpiScores {
   float* s = nullptr;
   float* d = nullptr;
   int h = 0, k = 0;
+  // fused ReLU (dense.hpp:197-228 activation / :232-268 backward), row-major
+  // n x N byte masks: relu_out -> out = max(out + bias, 0) and mask = (x > 0);
+  // mask_in -> out = mask ? out : 0 (the activation's backward)
+  uint8_t* relu_out = nullptr;
+  const uint8_t* mask_in = nullptr;
 };
 
 template <int BN>
@@ -519,6 +524,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
           const int col0 = n0 + c;
+          uint4 mk[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+          const bool mrow = row < M && col0 < N;  // masks need N % 32 == 0 (host)
+          if (sc.mask_in && mrow) {
+            const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * N + col0);
+            mk[0] = __ldg(mp);
+            mk[1] = __ldg(mp + 1);
+          }
+          uint32_t mo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
@@ -530,7 +543,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z = __fadd_rn(v.z, b.z);
               v.w = __fadd_rn(v.w, b.w);
             }
+            if (sc.relu_out) {
+              mo[j] = (v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 1u : 0u) << 8 |
+                      (v.z > 0.f ? 1u : 0u) << 16 | (v.w > 0.f ? 1u : 0u) << 24;
+              v.x = v.x > 0.f ? v.x : 0.f;
+              v.y = v.y > 0.f ? v.y : 0.f;
+              v.z = v.z > 0.f ? v.z : 0.f;
+              v.w = v.w > 0.f ? v.w : 0.f;
+            }
+            if (sc.mask_in) {
+              const uint32_t w = (&mk[j >> 2].x)[j & 3];
+              v.x = (w & 0xffu) ? v.x : 0.f;
+              v.y = (w & 0xff00u) ? v.y : 0.f;
+              v.z = (w & 0xff0000u) ? v.z : 0.f;
+              v.w = (w & 0xff000000u) ? v.w : 0.f;
+            }
             *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+          }
+          if (sc.relu_out && mrow) {
+            uint4* mp = reinterpret_cast<uint4*>(sc.relu_out + (int64_t)row * N + col0);
+            mp[0] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
+            mp[1] = make_uint4(mo[4], mo[5], mo[6], mo[7]);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -732,7 +765,7 @@ static bool tc_disabled() {
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src, const float* att_dst, float* s_out,
-                 float* d_out, int heads) {
+                 float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
@@ -790,9 +823,16 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     sc.h = heads;
     sc.k = hk;
   }
+  sc.relu_out = relu_out;
+  sc.mask_in = mask_in;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
   const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));
   if (!tma_store) mp.c = mp.a;  // unused
+  if (relu_out || mask_in) {  // fused ReLU / ReLU backward: TMA-store epilogue, whole 32-col chunks
+    if (!tma_store || (N & 31) != 0 || (reinterpret_cast<uintptr_t>(relu_out) & 15) ||
+        (reinterpret_cast<uintptr_t>(mask_in) & 15))
+      return false;
+  }
   if (pre) {
     k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
         belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);

@@ -71,6 +71,21 @@ bool gemm_scores_f32(sgnn_ctx ctx, const float* X, int32_t n, int32_t m, const f
                      int32_t hk, float* M, const float* a_src, const float* a_dst, int32_t h,
                      float* s, float* d);
 
+bool gemm_relu_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                   int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
+                   uint8_t* relu_out, const uint8_t* mask_in);
+
+// GCN layer calls of the models with ReLU fused where the producing kernel is
+// a tcgen05 GEMM (else a separate activation pass): forward writes the mask
+// and applies ReLU to out; backward applies the ReLU backward (mask_in) to
+// d_input.  gcn.cu.
+int gcn_forward_relu(sgnn_ctx ctx, sgnn_adj A, const void* X, int32_t m, const void* theta,
+                     const void* bias, int32_t k, const sgnn_scheme* s, void* out,
+                     sgnn_gcn_cache* cache, uint8_t* relu_mask);
+int gcn_backward_relu(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* theta, int32_t m,
+                      int32_t k, sgnn_gcn_cache c, int fg, void* d_theta, void* d_bias,
+                      void* d_input, const uint8_t* relu_mask_in);
+
 // C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,

@@ -150,15 +150,15 @@ void gcn2_step(sgnn_ctx ctx, sgnn_model md, sgnn_adj A, const T* X, const T* tar
   if (!out) o2 = DevBuf((size_t)n * k * sizeof(T), st);
   T* o = out ? out : o2.as<T>();
   GcnCacheGuard c1, c2;
-  ok(sgnn_gcn_forward(ctx, A, X, m, th1, b1, hid, &s1, h.get(), &c1.c));
-  act_fwd<T>(ctx, 0, (int64_t)n * hid, h.as<T>(), h.as<T>(), mask.as<uint8_t>());  // in place
+  // layer 1 with its ReLU (fused into the P.Theta / X.Theta epilogue when possible)
+  ok(gcn_forward_relu(ctx, A, X, m, th1, b1, hid, &s1, h.get(), &c1.c, mask.as<uint8_t>()));
   ok(sgnn_gcn_forward(ctx, A, h.get(), hid, th2, b2, k, &s2, o, &c2.c));
   DevBuf g((size_t)n * k * sizeof(T), st), dl(sizeof(double), st);
   mse<T>(ctx, (int64_t)n * k, o, target, g.as<T>(), loss ? loss : dl.as<double>());
   DevBuf dh((size_t)n * hid * sizeof(T), st);
-  ok(sgnn_gcn_backward(ctx, A, g.get(), th2, hid, k, c2.c, 1, grads[2], grads[3], dh.get()));
-  act_bwd<T>(ctx, 0, (int64_t)n * hid, dh.as<T>(), mask.as<uint8_t>(), (const T*)nullptr,
-             dh.as<T>());
+  // layer 2 backward with the ReLU backward applied to its input gradient
+  ok(gcn_backward_relu(ctx, A, g.get(), th2, hid, k, c2.c, 1, grads[2], grads[3], dh.get(),
+                       mask.as<uint8_t>()));
   ok(sgnn_gcn_backward(ctx, A, dh.get(), th1, m, hid, c1.c, cf.input_grad, grads[0], grads[1],
                        cf.input_grad ? d_input : nullptr));
 }
