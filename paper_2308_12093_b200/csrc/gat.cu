@@ -579,7 +579,16 @@ static int v2_R(int32_t h, int32_t k) {
   if (!(h == 1 || h == 2 || h == 4 || h == 8) || k % 4 != 0) return 0;
   int R = pick_r(h * k / 4);
   if (h == 8 && R == 4 && h * k / 4 <= 96) R = 3;  // 257..384 wide: 3 vectors per lane
-  return R <= 8 ? R : 0;
+  if (R <= 8) return R;
+  // wider slabs: 1024-float column windows (gridDim.y), heads whole per window
+  return 256 % (k / 4) == 0 ? 8 : 0;
+}
+
+// column windows of the dense-row gather kernels: slabs wider than 32R vectors
+template <class T>
+static unsigned v2_windows(int32_t h, int32_t k) {
+  const int fv = h * k / 4, R = v2_R<T>(h, k);
+  return (unsigned)((fv + 32 * R - 1) / (32 * R));
 }
 
 // (H, R) -> constexpr instantiation; R <= 32 * H / 32 lanes' worth
@@ -591,6 +600,9 @@ static int v2_R(int32_t h, int32_t k) {
     case 4 * 16 + 1: { constexpr int HH = 4, RR = 1; __VA_ARGS__; } break;          \
     case 4 * 16 + 2: { constexpr int HH = 4, RR = 2; __VA_ARGS__; } break;          \
     case 4 * 16 + 4: { constexpr int HH = 4, RR = 4; __VA_ARGS__; } break;          \
+    case 4 * 16 + 8: { constexpr int HH = 4, RR = 8; __VA_ARGS__; } break;          \
+    case 2 * 16 + 8: { constexpr int HH = 2, RR = 8; __VA_ARGS__; } break;          \
+    case 1 * 16 + 8: { constexpr int HH = 1, RR = 8; __VA_ARGS__; } break;          \
     case 8 * 16 + 1: { constexpr int HH = 8, RR = 1; __VA_ARGS__; } break;          \
     case 8 * 16 + 2: { constexpr int HH = 8, RR = 2; __VA_ARGS__; } break;          \
     case 8 * 16 + 3: { constexpr int HH = 8, RR = 3; __VA_ARGS__; } break;          \
@@ -659,7 +671,7 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
     HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, ci, sp, dp, (float)beta, ap, mp)));
     launched(ctx);
-    HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, ap, M4, k,
+    HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(n, rp, ci, ap, M4, k,
                                                                         b4, o4)));
     launched(ctx);
   } else if (R && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
@@ -797,10 +809,10 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const uint8_t* mk = cached ? c->mask.as<uint8_t>() : mask_t.as<uint8_t>();
     const int L = k / 4;
     if ((L & (L - 1)) == 0 && L <= 32) {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<v2_grid(n), 256, 0, st>>>(
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
                            n, rp, ci, M4, G4, k, da.as<float>())));
     } else {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<v2_grid(n), 256, 0, st>>>(
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
                            n, rp, ci, M4, G4, k, da.as<float>())));
     }
     launched(ctx);
@@ -808,7 +820,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
                          n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
                          dS.as<float>())));
     launched(ctx);
-    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<v2_grid(n), 256, 0, st>>>(
+    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
                          n, p->colptr.as<int32_t>(), p->rows.as<int32_t>(), p->perm.as<int32_t>(),
                          G4, al, dy.as<float>(), dS.as<float>(),
                          reinterpret_cast<const float4*>(a_src),
@@ -820,10 +832,10 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
       const int32_t chunk = (int32_t)ceil_div(n, nb);
       DevBuf part((size_t)nb * 3 * hk * sizeof(double), st);
       switch (h) {
-        case 1: g2::k_grads3_partial<1><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
-        case 2: g2::k_grads3_partial<2><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
-        case 4: g2::k_grads3_partial<4><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
-        default: g2::k_grads3_partial<8><<<nb, 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        case 1: g2::k_grads3_partial<1><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        case 2: g2::k_grads3_partial<2><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        case 4: g2::k_grads3_partial<4><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
+        default: g2::k_grads3_partial<8><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
       }
       launched(ctx);
       g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(
@@ -1151,7 +1163,7 @@ int sgnn_gat_aggregate(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, cons
   block_check(h, k);
   if (n_rows == 0) return SGNN_OK;
   const int R2 = v2_R<float>(h, k);
-  HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+  HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
                        n_rows, rowptr, cols, alpha, reinterpret_cast<const float4*>(M), k,
                        reinterpret_cast<const float4*>(bias), reinterpret_cast<float4*>(out))));
   launched(ctx);
@@ -1169,10 +1181,10 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
   const float4* M4 = reinterpret_cast<const float4*>(M);
   const float4* G4 = reinterpret_cast<const float4*>(G);
   if ((L & (L - 1)) == 0 && L <= 32) {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
                          n_rows, rowptr, cols, M4, G4, k, da)));
   } else {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<v2_grid(n_rows), 256, 0, ctx->stream>>>(
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
                          n_rows, rowptr, cols, M4, G4, k, da)));
   }
   launched(ctx);
@@ -1204,7 +1216,7 @@ int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
   block_check(h, k);
   if (n_cols == 0) return SGNN_OK;
   const int R2 = v2_R<float>(h, k);
-  HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<v2_grid(n_cols), 256, 0, ctx->stream>>>(
+  HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n_cols), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
                        n_cols, colptr, rows, perm, reinterpret_cast<const float4*>(G), alpha, dy,
                        dS, reinterpret_cast<const float4*>(a_src),
                        reinterpret_cast<const float4*>(a_dst), k, dD,
@@ -1234,10 +1246,10 @@ int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, con
   const float4* G4 = reinterpret_cast<const float4*>(G);
   const float4* M4 = reinterpret_cast<const float4*>(M);
   switch (h) {
-    case 1: g2::k_grads3_partial<1><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
-    case 2: g2::k_grads3_partial<2><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
-    case 4: g2::k_grads3_partial<4><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
-    default: g2::k_grads3_partial<8><<<nb, 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    case 1: g2::k_grads3_partial<1><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    case 2: g2::k_grads3_partial<2><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    case 4: g2::k_grads3_partial<4><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
+    default: g2::k_grads3_partial<8><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
   }
   launched(ctx);
   g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(

@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
                const float4* __restrict__ bias, float4* __restrict__ out) {
   constexpr int U = R >= 4 ? 1 : 2;
   const int lane = threadIdx.x & 31;
+  const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
   float4 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    tr[r] = min(H - 1, (r * 32 + lane) / L);
+    tr[r] = min(H - 1, (vo + r * 32 + lane) / L);
     acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   int32_t e = beg;
@@ -434,27 +435,27 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t v = r * 32 + lane;
+        const uint32_t v = vo + r * 32 + lane;
         if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
+        if (vo + r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
   }
   for (; e < end; ++e) {
     const uint32_t c = (uint32_t)__ldg(cols + e);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t v = r * 32 + lane;
+      const uint32_t v = vo + r * 32 + lane;
       if (v < (uint32_t)fv)
         fma4(acc[r], __ldg(alpha + (int64_t)e * H + tr[r]), __ldg(M + c * (uint32_t)fv + v));
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int v = r * 32 + lane;
+    const int v = vo + r * 32 + lane;
     if (v < fv) {
       const float4 b = __ldg(bias + v);
       float4 o = acc[r];
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
   constexpr int U = R >= 4 ? 1 : 2;
   __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
   float4 g[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int v = r * 32 + lane;
+    const int v = vo + r * 32 + lane;
     tr[r] = min(H - 1, v / L);
     g[r] = v < fv ? __ldg(G + (int64_t)i * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -506,14 +508,14 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t v = r * 32 + lane;
+        const uint32_t v = vo + r * 32 + lane;
         if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float p[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) p[r] = r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
+      for (int r = 0; r < R; ++r) p[r] = vo + r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
       if constexpr (P2) {
         for (int o = L >> 1; o > 0; o >>= 1)
 #pragma unroll
@@ -521,20 +523,21 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
         if (lead && e + u < end)
 #pragma unroll
           for (int r = 0; r < R; ++r)
-            if (r * 32 + lane < fv) da[(int64_t)(e + u) * H + tr[r]] = p[r];
+            if (vo + r * 32 + lane < fv) da[(int64_t)(e + u) * H + tr[r]] = p[r];
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (r * 32 + lane < fv) sh_p[wib][u][r * 32 + lane] = p[r];
+          if (vo + r * 32 + lane < fv) sh_p[wib][u][r * 32 + lane] = p[r];
       }
     }
     if constexpr (!P2) {
       __syncwarp();
-      if (lane < U * H) {
-        const int u = lane / H, t = lane % H;
+      const int hw = min(H, (32 * R) / L);  // heads of this window (whole: L | 32R)
+      if (lane < U * hw) {
+        const int u = lane / hw, tl = lane % hw, t = vo / L + tl;
         float acc = 0.f;
-        for (int q = 0; q < L; ++q) acc += sh_p[wib][u][t * L + q];
-        if (e + u < end) da[(int64_t)(e + u) * H + t] = acc;
+        for (int q = 0; q < L; ++q) acc += sh_p[wib][u][tl * L + q];
+        if (e + u < end && t < H) da[(int64_t)(e + u) * H + t] = acc;
       }
       __syncwarp();
     }
@@ -631,6 +634,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
     float* __restrict__ dD, float4* __restrict__ dM) {
   constexpr int U = R >= 4 ? 1 : 2;
   const int lane = threadIdx.x & 31;
+  const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (j >= n) return;
   const int fv = H * k / 4, L = k / 4;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
   float dd[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    tr[r] = min(H - 1, (r * 32 + lane) / L);
+    tr[r] = min(H - 1, (vo + r * 32 + lane) / L);
     acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     dd[r] = 0.f;
   }
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const uint32_t v = r * 32 + lane;
+        const uint32_t v = vo + r * 32 + lane;
         a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
         dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
         if (v < (uint32_t)fv) x[u][r] = __ldg(G + row[u] * (uint32_t)fv + v);
@@ -668,14 +672,14 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
+        if (vo + r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
   }
   for (; p < end; ++p) {
     const int32_t e = __ldg(perm + p);
     const uint32_t row = (uint32_t)__ldg(crows + p);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t v = r * 32 + lane;
+      const uint32_t v = vo + r * 32 + lane;
       const float a = __ldg(alpha + (int64_t)e * H + tr[r]);
       dd[r] += __ldg(dy + (int64_t)e * H + tr[r]);
       if (v < (uint32_t)fv) fma4(acc[r], a, __ldg(G + row * (uint32_t)fv + v));
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int v = r * 32 + lane;
+    const int v = vo + r * 32 + lane;
     if (v < fv) {
       if (v % L == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
       const float cs = __ldg(dS + (int64_t)j * H + tr[r]);
@@ -713,8 +717,9 @@ __global__ void __launch_bounds__(256) k_grads3_partial(int32_t n, int32_t k,
                                                         int32_t chunk, double* __restrict__ part) {
   __shared__ double sh[3][256][4];
   const int fv = H * k / 4, L = k / 4;
-  const int groups = max(1, 256 / fv);
-  const int tid = threadIdx.x, v = tid % fv, grp = tid / fv;
+  const int fvw = min(fv, 256);  // vectors of this column window (gridDim.y windows)
+  const int groups = max(1, 256 / fvw);
+  const int tid = threadIdx.x, v = blockIdx.y * 256 + tid % fvw, grp = tid / fvw;
   const int t = min(H - 1, v / L);
   const int32_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   double a[3][4] = {};
@@ -748,7 +753,7 @@ __global__ void __launch_bounds__(256) k_grads3_partial(int32_t n, int32_t k,
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) a[q][c] += sh[q][gg * fv + v][c];
+        for (int c = 0; c < 4; ++c) a[q][c] += sh[q][gg * fvw + tid % fvw][c];
     double* o = part + (int64_t)blockIdx.x * 3 * fv * 4;
 #pragma unroll
     for (int q = 0; q < 3; ++q)
