@@ -228,7 +228,9 @@ struct Cfg {
 //               a TMEM A buffer (no smem write-back); splits B in smem if needed
 //   warps 6..9  epilogue: TMEM -> registers -> (+bias) -> global, overlapping
 //               the next tile's MMAs
-template <bool A_MN, bool B_MN, int BN, bool B_PRE>
+// EPI: compile-time epilogue extras (the plain GEMM pays nothing for them):
+// bit 0 node scores, bit 1 ReLU + mask out, bit 2 ReLU backward (mask in)
+template <bool A_MN, bool B_MN, int BN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
-        if (sc.a_src != nullptr && n0 + c < N) {
+        if ((EPI & 1) && n0 + c < N) {
           // s[i,t] = sum_c a_src[t,c] M[i,tk+c] (kernels.hpp:385-423): a_src is h x k
           // row-major, so its flat index is the output column; k % 32 == 0 and
           // BN % k == 0, so a head is whole within this tile
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int col0 = n0 + c;
           uint4 mk[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
           const bool mrow = row < M && col0 < N;  // masks need N % 32 == 0 (host)
-          if (sc.mask_in && mrow) {
+          if ((EPI & 4) && mrow) {
             const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * N + col0);
             mk[0] = __ldg(mp);
             mk[1] = __ldg(mp + 1);
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z = __fadd_rn(v.z, b.z);
               v.w = __fadd_rn(v.w, b.w);
             }
-            if (sc.relu_out) {
+            if (EPI & 2) {
               mo[j] = (v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 1u : 0u) << 8 |
                       (v.z > 0.f ? 1u : 0u) << 16 | (v.w > 0.f ? 1u : 0u) << 24;
               v.x = v.x > 0.f ? v.x : 0.f;
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z = v.z > 0.f ? v.z : 0.f;
               v.w = v.w > 0.f ? v.w : 0.f;
             }
-            if (sc.mask_in) {
+            if (EPI & 4) {
               const uint32_t w = (&mk[j >> 2].x)[j & 3];
               v.x = (w & 0xffu) ? v.x : 0.f;
               v.y = (w & 0xff00u) ? v.y : 0.f;
@@ -560,7 +562,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
           }
-          if (sc.relu_out && mrow) {
+          if ((EPI & 2) && mrow) {
             uint4* mp = reinterpret_cast<uint4*>(sc.relu_out + (int64_t)row * N + col0);
             mp[0] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
             mp[1] = make_uint4(mo[4], mo[5], mo[6], mo[7]);
@@ -706,11 +708,11 @@ struct Maps {
   CUtensorMap a, b, blo, c;
 };
 
-template <bool A_MN, bool B_MN, int BN, bool B_PRE>
+template <bool A_MN, bool B_MN, int BN, bool B_PRE, int EPI>
 static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits, int kchunk,
                    float* C, const float* bias, float* part, int tma_store, float* cs_part,
                    const EpiScores& sc) {
-  auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE>;
+  auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE, EPI>;
   const int smem = Cfg<BN>::SMEM;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -730,7 +732,24 @@ static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& m
                      int K, int splits, int kchunk, float* C, const float* bias, float* part,
                      int tma_store, float* cs_part, const EpiScores& sc) {
 #define L(AM, BM_, PR) \
-  launch<AM, BM_, BN, PR>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc)
+  launch<AM, BM_, BN, PR, 0>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc)
+  // epilogue extras: only the shapes that use them are instantiated (the
+  // caller checked a_mn == false and pre == true)
+  if (sc.a_src) {
+    if (b_mn) launch<false, true, BN, true, 1>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 1>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
+  if (sc.relu_out) {
+    if (b_mn) launch<false, true, BN, true, 2>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 2>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
+  if (sc.mask_in) {
+    if (b_mn) launch<false, true, BN, true, 4>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 4>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
   if (pre) {
     if (a_mn && b_mn) L(true, true, true);
     else if (a_mn) L(true, false, true);
@@ -825,6 +844,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   }
   sc.relu_out = relu_out;
   sc.mask_in = mask_in;
+  if ((sc.a_src || relu_out || mask_in) && (a_mn || !pre)) return false;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
   const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));
   if (!tma_store) mp.c = mp.a;  // unused

@@ -57,11 +57,14 @@ def one_step(ls):
 def gat_step(ls):
     """One GAT layer step of scripts/kbench.py gat: X.Theta GEMM (+ split),
     node scores, ... up to the next step's GEMM.  Take the last complete one."""
-    idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores" in n]
-    if len(idx) < 2:
+    # the node scores live in the X.Theta epilogue: a step starts two launches
+    # (Theta split + GEMM) before its first attention kernel
+    idx = [i for i, (n, _) in enumerate(ls) if "k_gat_attn" in n]
+    if len(idx) < 3:
         return []
-    a, b = idx[-2], idx[-1]
-    return ls[a - 2:b - 2]
+    a, b = idx[-3], idx[-2]  # a complete step: attention (fwd) .. next step's split
+    fwd = [i for i in idx if a <= i < b]
+    return ls[a - 2:b - 2] if len(fwd) <= 1 else ls[a - 2:fwd[1] - 2]
 
 
 def main():
