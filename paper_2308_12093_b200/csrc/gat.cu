@@ -828,7 +828,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
                          reinterpret_cast<float4*>(dM.get()))));
     launched(ctx);
     {  // d_bias, d_a_src, d_a_dst: one pass over dX' and M
-      const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(2 * ctx->num_sms, n));
+      const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(4 * ctx->num_sms, n));
       const int32_t chunk = (int32_t)ceil_div(n, nb);
       DevBuf part((size_t)nb * 3 * hk * sizeof(double), st);
       switch (h) {
@@ -1240,7 +1240,7 @@ int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, con
     return SGNN_OK;
   }
   cudaStream_t st = ctx->stream;
-  const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(2 * ctx->num_sms, n_rows));
+  const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(4 * ctx->num_sms, n_rows));
   const int32_t chunk = (int32_t)ceil_div(n_rows, nb);
   DevBuf part((size_t)nb * 3 * hk * sizeof(double), st);
   const float4* G4 = reinterpret_cast<const float4*>(G);

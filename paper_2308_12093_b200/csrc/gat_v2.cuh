@@ -724,6 +724,7 @@ __global__ void __launch_bounds__(256) k_grads3_partial(int32_t n, int32_t k,
   const int32_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   double a[3][4] = {};
   if (grp < groups && v < fv) {
+#pragma unroll 2
     for (int32_t i = r0 + grp; i < r1; i += groups) {
       const float4 g = __ldg(G + (int64_t)i * fv + v);
       const float4 mm = __ldg(M + (int64_t)i * fv + v);

@@ -504,11 +504,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // row-major, so its flat index is the output column; k % 32 == 0 and
           // BN % k == 0, so a head is whole within this tile
           const int col0 = n0 + c;
+          const float4* as4 = reinterpret_cast<const float4*>(sc.a_src + col0);
+          const float4* ad4 = reinterpret_cast<const float4*>(sc.a_dst + col0);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float mv = __uint_as_float(r[j]);
-            ss = fmaf(mv, __ldg(sc.a_src + col0 + j), ss);
-            sd = fmaf(mv, __ldg(sc.a_dst + col0 + j), sd);
+          for (int j = 0; j < 8; ++j) {  // warp-uniform 16-byte loads (L1 broadcast)
+            const float4 as = __ldg(as4 + j), ad = __ldg(ad4 + j);
+            const float m0 = __uint_as_float(r[4 * j]), m1 = __uint_as_float(r[4 * j + 1]);
+            const float m2 = __uint_as_float(r[4 * j + 2]), m3 = __uint_as_float(r[4 * j + 3]);
+            ss = fmaf(m3, as.w, fmaf(m2, as.z, fmaf(m1, as.y, fmaf(m0, as.x, ss))));
+            sd = fmaf(m3, ad.w, fmaf(m2, ad.z, fmaf(m1, ad.y, fmaf(m0, ad.x, sd))));
           }
           if ((col0 + 32) % sc.k == 0) {
             if (row < M) {
