@@ -318,6 +318,30 @@ def run_ours(args):
 
     gat_ms = statistics.mean(timed(d.StepGraph(gat_step, ctx).replay, max(3, args.steps), 2))
 
+    # ---- the GAT layer's semibatched SDDMM alone (kernels.hpp:342-377) -------
+    # dAlpha[e, t] = <dX'[i, t, :], M[col_e, t, :]> over the pattern, h=8 k=32:
+    # algorithmic bytes 4(n+1) + 4q' (CSR) + 4n.hk (dX' once) + 4n.hk (M once) + 4q'h
+    from paper_2308_12093_b200 import _capi as capi
+    pa = P.arrays()
+    Mg = d.random_uniform(n, GAT_H * GAT_K, SEED + 21, ctx=ctx)
+    da = torch.empty((P.nnz, GAT_H), dtype=torch.float32, device=dev)
+
+    def sddmm():
+        capi.check(capi.lib.sgnn_gat_sddmm(ctx.handle, n, pa["rowptr"].data_ptr(),
+                                           pa["cols"].data_ptr(), GAT_H, GAT_K, Mg.data_ptr(),
+                                           Gg.data_ptr(), da.data_ptr()))
+
+    sd_ms = statistics.mean(timed(sddmm, reps, 2))
+    hk = GAT_H * GAT_K
+    sd_bytes = 4 * (n + 1) + 4 * P.nnz + 8 * n * hk + 4 * P.nnz * GAT_H
+    sd_gbs = sd_bytes / (sd_ms * 1e-3) / 1e9
+    sddmm_line = {"kernel": "g2::k_gat_sddmm2 (h=8, k=32, Arxiv pattern)", "ms": round(sd_ms, 4),
+                  "algorithmic_bytes": sd_bytes, "achieved": round(sd_gbs, 1), "peak": hbm,
+                  "unit": "GB/s", "frac": round(sd_gbs / hbm, 4),
+                  "gathered_bytes": P.nnz * hk * 4,
+                  "gather_frac_of_173MB_probe": round(P.nnz * hk * 4 / (sd_ms * 1e-3) / 1e9
+                                                      / 8561.0, 4)}
+
     # ---- 2-layer models, full training step with MSE (config 4) -------------
     gcn2 = d.Model("gcn2", M_IN, GCN2_HID, MODEL_OUT, scheme="adaptive", caching=True,
                    seed=SEED + 13, ctx=ctx)
@@ -398,6 +422,7 @@ def run_ours(args):
         "breakdown_ms": {k: round(v, 4) for k, v in comps.items()},
         "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K, "level": "full",
                       "nnz": P.nnz},
+        "sddmm": sddmm_line,
         "models": models,
         "setup_s": round(setup_s, 2),
     }
