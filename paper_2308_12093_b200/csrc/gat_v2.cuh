@@ -511,6 +511,43 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
         const uint32_t v = vo + r * 32 + lane;
         if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
       }
+    if (P2 && U * R <= L) {
+      // transposed reduction: the U*R partial dots of a lane are reduced over
+      // the L lanes of its head by a reduce-scatter (each step halves the live
+      // values) -- log2(U*R) + ... shuffles instead of U*R*log2(L); lane bits
+      // above the remaining xor range then name the (edge, chunk) it holds
+      constexpr int NV = U * R;
+      float p[NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          p[u * R + r] = vo + r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
+      int off = L >> 1;
+#pragma unroll
+      for (int half = NV / 2; half >= 1; half >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+          const float send = up ? p[q] : p[q + half];
+          const float keep = up ? p[q + half] : p[q];
+          p[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      for (; off > 0; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
+      // value index held: bits of (lane & (L/2 .. L/NV)) from the top down
+      int idx = 0;
+      {
+        int o2 = L >> 1;
+#pragma unroll
+        for (int half = NV / 2; half >= 1; half >>= 1, o2 >>= 1)
+          if (lane & o2) idx += half;
+      }
+      const int u = idx / R, r = idx % R;
+      if ((lane & ((L / NV) - 1)) == 0 && e + u < end && vo + r * 32 + lane < fv)
+        da[(int64_t)(e + u) * H + min(H - 1, (vo + r * 32 + lane) / L)] = p[0];
+      continue;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float p[R];
