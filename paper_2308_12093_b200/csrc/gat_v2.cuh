@@ -898,14 +898,18 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
     mx[t] = -INFINITY;
     sm[t] = 0.f;
   }
+  uint32_t pos1 = 0;  // mask bits of the lane's edge (single-pass rows)
   for (int32_t off = 0; off < wdeg; off += GS) {  // max
     const int32_t e = beg + off + gl;
     if (off + gl < deg) {
       float dj[H];
       ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+      pos1 = 0;
 #pragma unroll
       for (int t = 0; t < H; ++t) {
-        w[t] = lrelu(si[t] + dj[t], beta);
+        const float y = si[t] + dj[t];
+        if (y > 0.f) pos1 |= 1u << t;
+        w[t] = lrelu(y, beta);
         mx[t] = fmaxf(mx[t], w[t]);
       }
     }
@@ -931,14 +935,21 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
   for (int32_t off = 0; off < wdeg; off += GS) {  // alpha, mask
     const int32_t e = beg + off + gl;
     if (off + gl < deg) {
-      float dj[H], a[H];
-      uint32_t pos = 0;
-      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+      float a[H];
+      uint32_t pos = pos1;
+      if (one) {  // scores still in registers: no second gather
 #pragma unroll
-      for (int t = 0; t < H; ++t) {
-        const float y = si[t] + dj[t];
-        if (y > 0.f) pos |= 1u << t;
-        a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+        for (int t = 0; t < H; ++t) a[t] = __expf(w[t] - mx[t]) * sm[t];
+      } else {
+        float dj[H];
+        pos = 0;
+        ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+        for (int t = 0; t < H; ++t) {
+          const float y = si[t] + dj[t];
+          if (y > 0.f) pos |= 1u << t;
+          a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+        }
       }
       st_heads<H>(alpha + (int64_t)e * H, a);
       if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
