@@ -139,6 +139,17 @@ int sgnn_gcn_params_init(sgnn_ctx ctx, int32_t m, int32_t k, uint64_t seed, int 
 int sgnn_gat_params_init(sgnn_ctx ctx, int32_t m, int32_t h, int32_t k, uint64_t seed,
                          int dtype, void* theta, void* a_src, void* a_dst, void* bias);
 
+/* Chung-Lu power-law graph on the device (no reference counterpart: the
+ * reference generator graph.hpp:160-190 is uniform; BASELINE config 5 asks for
+ * a power-law graph).  w_i = (i+1)^(-1/(exponent-1)); round(avg_degree*n/2)
+ * pair draws from the counter-based splitmix64 stream of seed; undirected,
+ * both directions, no self loops or duplicates, canonical order.  src / dst:
+ * device buffers of sgnn_powerlaw_graph_capacity(n, avg_degree) entries;
+ * *count receives the number written (synchronises the context stream). */
+int64_t sgnn_powerlaw_graph_capacity(int32_t n, double avg_degree);
+int sgnn_powerlaw_graph(sgnn_ctx ctx, int32_t n, double avg_degree, double exponent,
+                        uint64_t seed, int32_t* src, int32_t* dst, int64_t* count);
+
 /* ---- sparse-format layer, on device (sparse.hpp, pattern.hpp) ------------ */
 /* sparse.hpp:110-142 coo_from_triplets: range check, stable sort by (row,col),
  * duplicates keep the LAST value.  Outputs have capacity nnz. */

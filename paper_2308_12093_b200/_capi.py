@@ -114,6 +114,8 @@ _SIGS = {
     "sgnn_gat_column_pass": (INT, [VP, I32, VP, VP, VP, I32, I32, VP, VP, VP, VP, VP, VP, VP,
                                    VP]),
     "sgnn_gat_param_grads": (INT, [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP]),
+    "sgnn_powerlaw_graph_capacity": (I64, [I32, D]),
+    "sgnn_powerlaw_graph": (INT, [VP, I32, D, D, U64, VP, VP, PI64]),
     "sgnn_activation": (INT, [VP, INT, INT, VP, I64, VP, VP]),
     "sgnn_activation_backward": (INT, [VP, INT, INT, VP, VP, VP, I64, VP]),
     "sgnn_loss_mse": (INT, [VP, INT, VP, VP, I64, I64, VP, VP]),

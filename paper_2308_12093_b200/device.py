@@ -188,6 +188,19 @@ def synthetic_graph(n, avg_degree, seed):
     return src, dst
 
 
+def powerlaw_graph(n, avg_degree, exponent=3.0, seed=1, ctx=None):
+    """Chung-Lu power-law graph generated on the device (sgnn_powerlaw_graph):
+    int32 device tensors (src, dst), undirected, canonical order."""
+    ctx = _ctx(ctx)
+    cap = lib.sgnn_powerlaw_graph_capacity(n, float(avg_degree))
+    src = torch.empty(max(cap, 1), dtype=torch.int32, device=ctx.device)
+    dst = torch.empty(max(cap, 1), dtype=torch.int32, device=ctx.device)
+    cnt = C.c_int64()
+    check(lib.sgnn_powerlaw_graph(ctx.handle, n, float(avg_degree), float(exponent), seed,
+                                  _p(src), _p(dst), C.byref(cnt)))
+    return src[:cnt.value], dst[:cnt.value]
+
+
 # ---- sparse-format layer ---------------------------------------------------
 def _i32(t, dev):
     return t.to(device=dev, dtype=torch.int32).contiguous()
