@@ -15,6 +15,13 @@ using namespace sgnn;
 
 namespace {
 
+const LongRows* fwd_plan(sgnn_ctx ctx, sgnn_adj A) {
+  return &long_rows(ctx, A->long_fwd, A->n_rows, A->rowptr.as<int32_t>());
+}
+const LongRows* bwd_plan(sgnn_ctx ctx, sgnn_adj A) {
+  return &long_rows(ctx, A->long_bwd, A->n_cols, A->colptr.as<int32_t>());
+}
+
 inline void ok(int rc) {
   if (rc == SGNN_OK) return;
   if (rc == SGNN_EINVAL) throw invalid_argument(sgnn_last_error());
@@ -40,12 +47,12 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
   if (s.forward == SGNN_TRANSFORM_FIRST) {
     DevBuf M((size_t)n * k * sizeof(T), st);
     gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
-    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz);
+    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz, fwd_plan(ctx, A));
     if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
     c->saved_input = X;
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
-    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
+    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
     bool fused = false;
     if constexpr (sizeof(T) == 4)
       if (relu) fused = gemm_relu_f32(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias,
@@ -85,7 +92,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf S((size_t)n * k * sizeof(T), st);
       column_sums<T>(ctx, G, n, k, d_bias);
-      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz);
+      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bwd_plan(ctx, A));
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
       if (fg) {
         bool fused = false;
@@ -102,12 +109,13 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     case SGNN_SPLIT_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf P((size_t)n * m * sizeof(T), st);
-      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz);
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
       gemm_tn_colsum<T>(ctx, P.as<T>(), n, m, G, n, k, d_theta, d_bias);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
+                    bwd_plan(ctx, A));
         relu_bwd();
       }
       break;
@@ -118,7 +126,8 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
+                    bwd_plan(ctx, A));
         relu_bwd();
       }
       break;

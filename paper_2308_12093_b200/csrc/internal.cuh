@@ -4,6 +4,23 @@
 
 #include "common.cuh"
 
+namespace sgnn {
+// Rows longer than kLongRow edges (power-law hubs) are split into kLongRow-edge
+// segments, each on its own warp, combined in segment order: without it one
+// warp would walk a hub row alone while the rest of the GPU idles.  Built
+// once per operator (and direction) on first use.
+constexpr int32_t kLongRow = 512;
+struct LongRows {
+  bool built = false;
+  const int32_t* rowptr = nullptr;  // the CSR the plan belongs to
+  int32_t nseg = 0, nlong = 0;
+  DevBuf seg_beg, seg_end;  // nseg: edge range of every segment
+  DevBuf long_row;    // nlong: row id
+  DevBuf long_first;  // nlong + 1: first segment of every long row (+ sentinel)
+};
+LongRows& long_rows(sgnn_ctx ctx, LongRows& plan, int32_t n_rows, const int32_t* rowptr);
+}  // namespace sgnn
+
 // AdjacencyOp (kernels.hpp:191-211): forward CSR and the CSC arrays that are
 // the CSR of A^T (zero-copy transpose of sparse.hpp:400-420), owned here.
 struct sgnn_adj_s {
@@ -13,6 +30,7 @@ struct sgnn_adj_s {
   int format = SGNN_CSC;
   sgnn::DevBuf rowptr, cols, vals;    // CSR of A
   sgnn::DevBuf colptr, crows, cvals;  // CSC of A == CSR of A^T
+  sgnn::LongRows long_fwd, long_bwd;  // hub-row plans of the CSR / CSC
   ~sgnn_adj_s();
 };
 
@@ -89,7 +107,8 @@ int gcn_backward_relu(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* t
 // C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz);
+              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz,
+              const LongRows* lr = nullptr);
 
 // C = op(A) op(B) (row-major); A ra x ca, B rb x cb; bias added per column of C
 template <class T>

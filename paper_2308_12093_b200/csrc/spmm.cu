@@ -11,6 +11,8 @@
 // order with an unfused multiply then add (madd), which is exactly the
 // reference's `crow[c] += v * brow[c]` (kernels.hpp:47-51): results are
 // bit-identical to the reference CPU SpMM in float32 and float64.
+#include <cub/cub.cuh>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -205,16 +207,30 @@ __global__ void __launch_bounds__(256, (R == 1 && sizeof(T) == 4) ? SPMM_MINB : 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float4 ldB(const float4* p) { return __ldg(p); }
 
-template <int R, int U>
+// Rows longer than `longest` edges are skipped (a LongRows plan covers them).
+// SEG: the warp owns segment `row` of a long row instead: edges
+// [seg_beg[row], rowptr[row]) -- in SEG mode `rowptr` carries the segment
+// ends -- written without bias to its own partial row of C (combined in
+// segment order by k_spmm_combine).
+template <int R, int U, bool SEG = false>
 __global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 : 4)))
     k_spmm_lean(int32_t n_rows, const int32_t* __restrict__ rowptr,
                 const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 const float4* __restrict__ B, int32_t fv, float4* __restrict__ C,
-                const float4* __restrict__ bias, int32_t ldv) {
+                const float4* __restrict__ bias, int32_t ldv, int32_t longest = 0x7fffffff,
+                const int32_t* __restrict__ seg_beg = nullptr) {
   const int lane = threadIdx.x & 31;
   const int32_t row = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (row >= n_rows) return;
-  const int32_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  int32_t beg, end;
+  if (SEG) {
+    beg = __ldg(seg_beg + row);
+    end = __ldg(rowptr + row);
+  } else {
+    beg = __ldg(rowptr + row);
+    end = __ldg(rowptr + row + 1);
+    if (end - beg > longest) return;
+  }
   float4 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -266,7 +282,7 @@ __global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 
   for (int r = 0; r < R; ++r) {
     if ((r == 0 && ok0) || (r == 1 && ok1)) {
       float4 o = acc[r];
-      if (bias) {
+      if (!SEG && bias) {
         const float4 bb = __ldg(bias + r * 32 + lane);
         o.x = __fadd_rn(o.x, bb.x);
         o.y = __fadd_rn(o.y, bb.y);
@@ -278,20 +294,140 @@ __global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 
   }
 }
 
+// Long rows: sum the segment partials of each long row in segment order
+// (+ bias) -- warp per long row, lanes over 16-byte vectors.
+__global__ void __launch_bounds__(256) k_spmm_combine(int32_t nlong,
+                                                      const int32_t* __restrict__ long_row,
+                                                      const int32_t* __restrict__ long_first,
+                                                      const float4* __restrict__ part,
+                                                      int32_t fv, float4* __restrict__ C,
+                                                      const float4* __restrict__ bias,
+                                                      int32_t ldv) {
+  const int lane = threadIdx.x & 31;
+  const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (j >= nlong) return;
+  const int32_t row = __ldg(long_row + j), s0 = __ldg(long_first + j),
+                s1 = __ldg(long_first + j + 1);
+  for (int v = lane; v < fv; v += 32) {
+    float4 a = __ldg(part + (int64_t)s0 * fv + v);
+    for (int32_t s = s0 + 1; s < s1; ++s) {
+      const float4 b = __ldg(part + (int64_t)s * fv + v);
+      a.x = __fadd_rn(a.x, b.x);
+      a.y = __fadd_rn(a.y, b.y);
+      a.z = __fadd_rn(a.z, b.z);
+      a.w = __fadd_rn(a.w, b.w);
+    }
+    if (bias) {
+      const float4 bb = __ldg(bias + v);
+      a.x = __fadd_rn(a.x, bb.x);
+      a.y = __fadd_rn(a.y, bb.y);
+      a.z = __fadd_rn(a.z, bb.z);
+      a.w = __fadd_rn(a.w, bb.w);
+    }
+    C[(int64_t)row * ldv + v] = a;
+  }
+}
+
+__global__ void k_long_count(int32_t n, const int32_t* __restrict__ rowptr, int32_t seglen,
+                             int32_t* __restrict__ segs, int32_t* __restrict__ islong) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t deg = i < n ? rowptr[i + 1] - rowptr[i] : 0;
+    segs[i] = deg > seglen ? (deg + seglen - 1) / seglen : 0;
+    islong[i] = deg > seglen ? 1 : 0;
+  }
+}
+
+__global__ void k_long_fill(int32_t n, const int32_t* __restrict__ rowptr, int32_t seglen,
+                            const int32_t* __restrict__ segoff, const int32_t* __restrict__ longoff,
+                            int32_t* __restrict__ seg_beg, int32_t* __restrict__ seg_end,
+                            int32_t* __restrict__ long_row, int32_t* __restrict__ long_first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t beg = rowptr[i], end = rowptr[i + 1];
+    if (end - beg <= seglen) continue;
+    const int32_t j = longoff[i], s0 = segoff[i];
+    long_row[j] = (int32_t)i;
+    long_first[j] = s0;
+    int32_t s = s0;
+    for (int32_t e = beg; e < end; e += seglen, ++s) {
+      seg_beg[s] = e;
+      seg_end[s] = min(e + seglen, end);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) long_first[longoff[n]] = segoff[n];  // sentinel
+}
+
+LongRows& long_rows(sgnn_ctx ctx, LongRows& plan, int32_t n, const int32_t* rowptr) {
+  if (plan.built && plan.rowptr == rowptr) return plan;
+  cudaStream_t st = ctx->stream;
+  plan = LongRows();
+  plan.rowptr = rowptr;
+  plan.built = true;
+  if (n <= 0) return plan;
+  DevBuf segs((size_t)(n + 1) * 4, st), isl((size_t)(n + 1) * 4, st),
+      segoff((size_t)(n + 1) * 4, st), longoff((size_t)(n + 1) * 4, st);
+  k_long_count<<<grid_for(ctx, n + 1, 256), 256, 0, st>>>(n, rowptr, kLongRow, segs.as<int32_t>(),
+                                                          isl.as<int32_t>());
+  launched(ctx);
+  size_t tb = 0;
+  SGNN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, segs.as<int32_t>(), segoff.as<int32_t>(),
+                                          n + 1, st));
+  {
+    DevBuf t(tb, st);
+    SGNN_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tb, segs.as<int32_t>(),
+                                            segoff.as<int32_t>(), n + 1, st));
+    SGNN_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tb, isl.as<int32_t>(),
+                                            longoff.as<int32_t>(), n + 1, st));
+  }
+  int32_t cnt[2] = {0, 0};
+  SGNN_CUDA(cudaMemcpyAsync(&cnt[0], segoff.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
+  SGNN_CUDA(cudaMemcpyAsync(&cnt[1], longoff.as<int32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
+  SGNN_CUDA(cudaStreamSynchronize(st));  // once per operator
+  plan.nseg = cnt[0];
+  plan.nlong = cnt[1];
+  if (plan.nlong == 0) return plan;
+  plan.seg_beg = DevBuf((size_t)plan.nseg * 4, st);
+  plan.seg_end = DevBuf((size_t)plan.nseg * 4, st);
+  plan.long_row = DevBuf((size_t)plan.nlong * 4, st);
+  plan.long_first = DevBuf((size_t)(plan.nlong + 1) * 4, st);
+  k_long_fill<<<grid_for(ctx, n, 256), 256, 0, st>>>(n, rowptr, kLongRow, segoff.as<int32_t>(),
+                                                     longoff.as<int32_t>(), plan.seg_beg.as<int32_t>(),
+                                                     plan.seg_end.as<int32_t>(),
+                                                     plan.long_row.as<int32_t>(),
+                                                     plan.long_first.as<int32_t>());
+  launched(ctx);
+  return plan;
+}
+
 template <int R>
 static void launch_lean(sgnn_ctx ctx, int U, int32_t n_rows, const int32_t* rowptr,
                         const int32_t* cols, const float* vals, const float* B, int32_t f,
-                        float* C, const float* bias, int32_t ld) {
+                        float* C, const float* bias, int32_t ld, const LongRows* lr = nullptr) {
   const int grid = (int)ceil_div(n_rows, 8);
   const float4* Bv = reinterpret_cast<const float4*>(B);
   float4* Cv = reinterpret_cast<float4*>(C);
   const float4* bv = reinterpret_cast<const float4*>(bias);
+  const bool split = lr && lr->nlong > 0;
+  const int32_t longest = split ? kLongRow : 0x7fffffff;
   if (U >= 4)
-    k_spmm_lean<R, 4><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+    k_spmm_lean<R, 4><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4, longest);
   else if (U >= 2)
-    k_spmm_lean<R, 2><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+    k_spmm_lean<R, 2><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4, longest);
   else
-    k_spmm_lean<R, 1><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4);
+    k_spmm_lean<R, 1><<<grid, 256, 0, ctx->stream>>>(n_rows, rowptr, cols, vals, Bv, f / 4, Cv, bv, ld / 4, longest);
+  launched(ctx);
+  if (!split) return;
+  // long rows: kLongRow-edge segments on their own warps, then an in-order combine
+  DevBuf part((size_t)lr->nseg * f * 4, ctx->stream);
+  float4* pv = part.as<float4>();
+  k_spmm_lean<R, 2, true><<<(unsigned)ceil_div(lr->nseg, 8), 256, 0, ctx->stream>>>(
+      lr->nseg, lr->seg_end.as<int32_t>(), cols, vals, Bv, f / 4, pv, nullptr, f / 4, 0x7fffffff,
+      lr->seg_beg.as<int32_t>());
+  launched(ctx);
+  k_spmm_combine<<<(unsigned)ceil_div(lr->nlong, 8), 256, 0, ctx->stream>>>(
+      lr->nlong, lr->long_row.as<int32_t>(), lr->long_first.as<int32_t>(), pv, f / 4, Cv, bv,
+      ld / 4);
   launched(ctx);
 }
 
@@ -356,7 +492,8 @@ static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const 
 // the generic kernel (both are bit-identical to the reference).
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz) {
+              const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz,
+              const LongRows* lr) {
   if (n_rows == 0 || f == 0) return;
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;
   const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
@@ -367,8 +504,8 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
     static const int lu = getenv("SGNN_SPMM_U") ? atoi(getenv("SGNN_SPMM_U")) : 2;
     const bool vec_ok = aligned && f % 4 == 0 && nnz > 0;
     if (mode == 0 && vec_ok && f > 64 && f <= 256) {  // lean one-row-per-warp kernel
-      if (f <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f);
-      else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f);
+      if (f <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f, lr);
+      else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B, f, C, bias, f, lr);
       return;
     }
     if (mode == 0 && vec_ok && f > 256) {
@@ -377,8 +514,8 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
       for (int32_t c0 = 0; c0 < f; c0 += 256) {
         const int32_t w = f - c0 < 256 ? f - c0 : 256;
         const float* bw = bias ? bias + c0 : nullptr;
-        if (w <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f);
-        else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f);
+        if (w <= 128) launch_lean<1>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f, lr);
+        else launch_lean<2>(ctx, lu, n_rows, rowptr, cols, vals, B + c0, w, C + c0, bw, f, lr);
       }
       return;
     }
@@ -390,9 +527,11 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
 }
 
 template void spmm_csr<float>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const float*,
-                              const float*, int32_t, float*, const float*, int64_t);
+                              const float*, int32_t, float*, const float*, int64_t,
+                              const LongRows*);
 template void spmm_csr<double>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const double*,
-                               const double*, int32_t, double*, const double*, int64_t);
+                               const double*, int32_t, double*, const double*, int64_t,
+                               const LongRows*);
 
 }  // namespace sgnn
 
@@ -406,14 +545,15 @@ extern "C" int sgnn_spmm(sgnn_ctx ctx, sgnn_adj adj, int transposed, const void*
   const int32_t n_out = transposed ? adj->n_cols : adj->n_rows;
   const int32_t* ptr = transposed ? adj->colptr.as<int32_t>() : adj->rowptr.as<int32_t>();
   const int32_t* idx = transposed ? adj->crows.as<int32_t>() : adj->cols.as<int32_t>();
+  const LongRows* lr = &long_rows(ctx, transposed ? adj->long_bwd : adj->long_fwd, n_out, ptr);
   if (adj->dtype == SGNN_F32) {
     const float* v = transposed ? adj->cvals.as<float>() : adj->vals.as<float>();
     spmm_csr<float>(ctx, n_out, ptr, idx, v, static_cast<const float*>(B), f,
-                    static_cast<float*>(C), static_cast<const float*>(bias), adj->nnz);
+                    static_cast<float*>(C), static_cast<const float*>(bias), adj->nnz, lr);
   } else {
     const double* v = transposed ? adj->cvals.as<double>() : adj->vals.as<double>();
     spmm_csr<double>(ctx, n_out, ptr, idx, v, static_cast<const double*>(B), f,
-                     static_cast<double*>(C), static_cast<const double*>(bias), adj->nnz);
+                     static_cast<double*>(C), static_cast<const double*>(bias), adj->nnz, lr);
   }
   SGNN_API_END
 }
