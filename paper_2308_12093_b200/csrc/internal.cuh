@@ -9,7 +9,7 @@ namespace sgnn {
 // segments, each on its own warp, combined in segment order: without it one
 // warp would walk a hub row alone while the rest of the GPU idles.  Built
 // once per operator (and direction) on first use.
-constexpr int32_t kLongRow = 512;
+constexpr int32_t kLongRow = 128;
 struct LongRows {
   bool built = false;
   const int32_t* rowptr = nullptr;  // the CSR the plan belongs to
