@@ -613,6 +613,23 @@ static unsigned v2_windows(int32_t h, int32_t k) {
 
 static unsigned v2_grid(int32_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, g2::WPB)); }
 
+// hub rows / columns of a pattern (LongRows plan): segment arguments
+static g2::SegArgs seg_args(const LongRows& pl, float* part = nullptr, float* ddpart = nullptr) {
+  g2::SegArgs a;
+  a.longest = 0x7fffffff;
+  a.row = pl.seg_row.as<int32_t>();
+  a.beg = pl.seg_beg.as<int32_t>();
+  a.end = pl.seg_end.as<int32_t>();
+  a.part = reinterpret_cast<float4*>(part);
+  a.ddpart = ddpart;
+  return a;
+}
+static g2::SegArgs skip_long(const LongRows& pl) {
+  g2::SegArgs a;
+  a.longest = pl.nlong ? kLongRow : 0x7fffffff;
+  return a;
+}
+
 template <class T>
 static void node_scores_fast(sgnn_ctx ctx, int R, int32_t n, int32_t h, int32_t k, const T* M,
                              const T* a_src, const T* a_dst, T* s, T* d) {
@@ -668,12 +685,27 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
       alpha_tmp = DevBuf((size_t)q * h * sizeof(T) + 16, st);
       ap = alpha_tmp.as<float>();
     }
+    const LongRows& pr = long_rows(ctx, p->long_rows, n, rp);
+    const g2::SegArgs sk = skip_long(pr);
     HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
-                         n, rp, ci, sp, dp, (float)beta, ap, mp)));
+                         n, rp, ci, sp, dp, (float)beta, ap, mp, sk.longest)));
     launched(ctx);
+    if (pr.nlong) {  // hub rows: a block per row
+      HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
+                          pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta, ap, mp)));
+      launched(ctx);
+    }
     HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(n, rp, ci, ap, M4, k,
-                                                                        b4, o4)));
+                                                                        b4, o4, sk)));
     launched(ctx);
+    if (pr.nlong) {  // hub rows: segment partials, combined in order (+ bias)
+      DevBuf part((size_t)pr.nseg * hk * sizeof(float), st);
+      HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR, true><<<dim3(v2_grid(pr.nseg), v2_windows<T>(h, k)), 256, 0, st>>>(
+                           pr.nseg, rp, ci, ap, M4, k, b4, o4, seg_args(pr, part.as<float>()))));
+      launched(ctx);
+      spmm_combine(ctx, pr, part.as<float>(), hk, reinterpret_cast<float*>(out),
+                   reinterpret_cast<const float*>(bias), hk);
+    }
   } else if (R && al16(M.get()) && al16(out) && al16(bias) && al16(a_src) && al16(a_dst)) {
     constexpr int VW = sizeof(T) == 4 ? 4 : 2;
     constexpr int wpb = gf::WPB<T>::v;
@@ -799,34 +831,72 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const float4* G4 = reinterpret_cast<const float4*>(G);
     const float* sp = reinterpret_cast<const float*>(r.sp);
     const float* dp = reinterpret_cast<const float*>(r.dp);
+    const LongRows& pr = long_rows(ctx, p->long_rows, n, rp);
+    const LongRows& pc = long_rows(ctx, p->long_cols, n, p->colptr.as<int32_t>());
+    const g2::SegArgs sk = skip_long(pr), skc = skip_long(pc);
     if (!cached) {  // attention + mask recomputed like gat_recompute (gat.hpp:150-170)
       HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                            n, rp, ci, sp, dp, (float)beta, alpha_t.as<float>(),
-                           mask_t.as<uint8_t>())));
+                           mask_t.as<uint8_t>(), sk.longest)));
       launched(ctx);
+      if (pr.nlong) {
+        HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
+                            pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta,
+                            alpha_t.as<float>(), mask_t.as<uint8_t>())));
+        launched(ctx);
+      }
     }
     const float* al = reinterpret_cast<const float*>(alpha);
     const uint8_t* mk = cached ? c->mask.as<uint8_t>() : mask_t.as<uint8_t>();
     const int L = k / 4;
+    const unsigned wn = v2_windows<T>(h, k);
     if ((L & (L - 1)) == 0 && L <= 32) {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
-                           n, rp, ci, M4, G4, k, da.as<float>())));
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
+                           n, rp, ci, M4, G4, k, da.as<float>(), sk)));
+      if (pr.nlong)  // hub rows: per-edge outputs, segments write them directly
+        HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true, true><<<dim3(v2_grid(pr.nseg), wn), 256, 0, st>>>(
+                             pr.nseg, rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
     } else {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
-                           n, rp, ci, M4, G4, k, da.as<float>())));
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
+                           n, rp, ci, M4, G4, k, da.as<float>(), sk)));
+      if (pr.nlong)
+        HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false, true><<<dim3(v2_grid(pr.nseg), wn), 256, 0, st>>>(
+                             pr.nseg, rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
     }
     launched(ctx);
     HR_SWITCH(h, R2, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
-                         dS.as<float>())));
+                         dS.as<float>(), sk.longest)));
     launched(ctx);
-    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(
-                         n, p->colptr.as<int32_t>(), p->rows.as<int32_t>(), p->perm.as<int32_t>(),
-                         G4, al, dy.as<float>(), dS.as<float>(),
-                         reinterpret_cast<const float4*>(a_src),
-                         reinterpret_cast<const float4*>(a_dst), k, dD.as<float>(),
-                         reinterpret_cast<float4*>(dM.get()))));
+    if (pr.nlong) {
+      HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pr.nlong, 256, 0, st>>>(
+                          pr.long_row.as<int32_t>(), rp, al, mk, da.as<float>(), (float)beta,
+                          dy.as<float>(), dS.as<float>())));
+      launched(ctx);
+    }
+    const int32_t* cpp = p->colptr.as<int32_t>();
+    const int32_t* crw = p->rows.as<int32_t>();
+    const int32_t* prm = p->perm.as<int32_t>();
+    const float4* as4 = reinterpret_cast<const float4*>(a_src);
+    const float4* ad4 = reinterpret_cast<const float4*>(a_dst);
+    float4* dM4 = reinterpret_cast<float4*>(dM.get());
+    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
+                         n, cpp, crw, prm, G4, al, dy.as<float>(), dS.as<float>(), as4, ad4, k,
+                         dD.as<float>(), dM4, skc)));
     launched(ctx);
+    if (pc.nlong) {  // hub columns: segment partials + in-order combine
+      DevBuf part((size_t)pc.nseg * hk * sizeof(float), st), ddp((size_t)pc.nseg * h * 4, st);
+      HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true><<<dim3(v2_grid(pc.nseg), wn), 256, 0, st>>>(
+                           pc.nseg, cpp, crw, prm, G4, al, dy.as<float>(), dS.as<float>(), as4,
+                           ad4, k, dD.as<float>(), dM4,
+                           seg_args(pc, part.as<float>(), ddp.as<float>()))));
+      launched(ctx);
+      HR_SWITCH(h, 1, (g2::k_gat_col_combine<HH><<<v2_grid(pc.nlong), 256, 0, st>>>(
+                          pc.nlong, pc.long_row.as<int32_t>(), pc.long_first.as<int32_t>(),
+                          part.as<float4>(), ddp.as<float>(), dS.as<float>(), as4, ad4, k,
+                          dD.as<float>(), dM4)));
+      launched(ctx);
+    }
     {  // d_bias, d_a_src, d_a_dst: one pass over dX' and M
       const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(4 * ctx->num_sms, n));
       const int32_t chunk = (int32_t)ceil_div(n, nb);

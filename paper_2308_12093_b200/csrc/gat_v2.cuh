@@ -26,6 +26,19 @@ namespace g2 {
 
 constexpr int WPB = 8;  // warps (rows) per block
 
+// Hub rows / columns (a LongRows plan, internal.cuh): the row kernels skip rows
+// longer than `longest`; their SEG instantiation runs one warp per segment
+// (row[s], edges [beg[s], end[s])) and writes partials (combined in segment
+// order afterwards) or, for per-edge outputs, the final values directly.
+struct SegArgs {
+  int32_t longest = 0x7fffffff;
+  const int32_t* row = nullptr;
+  const int32_t* beg = nullptr;
+  const int32_t* end = nullptr;
+  float4* part = nullptr;  // nseg x fv partial rows
+  float* ddpart = nullptr; // nseg x h partial column sums (column pass)
+};
+
 // dense-row gathers in flight per warp: 4 16-byte vectors per lane in total
 template <int R>
 struct Unroll {
@@ -401,18 +414,26 @@ static inline unsigned attn3_grid(int32_t n) {
 // attention load per lane (its head; 32-byte sector per edge) and R 16-byte
 // row vectors, U edges in flight; <= 40 registers for 48 resident warps/SM.
 // ---------------------------------------------------------------------------
-template <int H, int R>
+template <int H, int R, bool SEG = false>
 __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
-               const float4* __restrict__ bias, float4* __restrict__ out) {
+               const float4* __restrict__ bias, float4* __restrict__ out, SegArgs sg = {}) {
   constexpr int U = R >= 4 ? 1 : 2;
   const int lane = threadIdx.x & 31;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
-  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  int32_t beg, end;
+  if (SEG) {
+    beg = __ldg(sg.beg + i);
+    end = __ldg(sg.end + i);
+  } else {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+    if (end - beg > sg.longest) return;
+  }
   int tr[R];
   float4 acc[R];
 #pragma unroll
@@ -457,6 +478,10 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
   for (int r = 0; r < R; ++r) {
     const int v = vo + r * 32 + lane;
     if (v < fv) {
+      if (SEG) {
+        sg.part[(int64_t)i * fv + v] = acc[r];
+        continue;
+      }
       const float4 b = __ldg(bias + v);
       float4 o = acc[r];
       o.x += b.x;
@@ -477,11 +502,11 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
 // per-vector partial dots go through shared memory and H*U lanes fold the
 // k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
-template <int H, int R, bool P2>
+template <int H, int R, bool P2, bool SEG = false>
 __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
     k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                  const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
-                 float* __restrict__ da) {
+                 float* __restrict__ da, SegArgs sg = {}) {
   constexpr int U = R >= 4 ? 1 : 2;
   __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -489,14 +514,23 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
-  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  int32_t beg, end, grow = i;  // grow: the row of dX' this warp dots against
+  if (SEG) {
+    beg = __ldg(sg.beg + i);
+    end = __ldg(sg.end + i);
+    grow = __ldg(sg.row + i);
+  } else {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+    if (end - beg > sg.longest) return;
+  }
   int tr[R];
   float4 g[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int v = vo + r * 32 + lane;
     tr[r] = min(H - 1, v / L);
-    g[r] = v < fv ? __ldg(G + (int64_t)i * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    g[r] = v < fv ? __ldg(G + (int64_t)grow * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const bool lead = P2 && (lane & (L - 1)) == 0;
   for (int32_t e = beg; e < end; e += U) {
@@ -662,20 +696,28 @@ __global__ void __launch_bounds__(256) k_gat_sbwd3(int32_t n, const int32_t* __r
 // lane (its head), the dX' row R 16-byte vectors; the lanes of a head carry
 // identical dD sums, so no reduction is needed.
 // ---------------------------------------------------------------------------
-template <int H, int R>
+template <int H, int R, bool SEG = false>
 __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
     int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
     const int32_t* __restrict__ perm, const float4* __restrict__ G,
     const float* __restrict__ alpha, const float* __restrict__ dy, const float* __restrict__ dS,
     const float4* __restrict__ a_src, const float4* __restrict__ a_dst, int32_t k,
-    float* __restrict__ dD, float4* __restrict__ dM) {
+    float* __restrict__ dD, float4* __restrict__ dM, SegArgs sg = {}) {
   constexpr int U = R >= 4 ? 1 : 2;
   const int lane = threadIdx.x & 31;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (j >= n) return;
   const int fv = H * k / 4, L = k / 4;
-  const int32_t beg = __ldg(colptr + j), end = __ldg(colptr + j + 1);
+  int32_t beg, end;
+  if (SEG) {
+    beg = __ldg(sg.beg + j);
+    end = __ldg(sg.end + j);
+  } else {
+    beg = __ldg(colptr + j);
+    end = __ldg(colptr + j + 1);
+    if (end - beg > sg.longest) return;
+  }
   int tr[R];
   float4 acc[R];
   float dd[R];
@@ -726,6 +768,11 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
   for (int r = 0; r < R; ++r) {
     const int v = vo + r * 32 + lane;
     if (v < fv) {
+      if (SEG) {
+        sg.part[(int64_t)j * fv + v] = acc[r];
+        if (v % L == 0) sg.ddpart[(int64_t)j * H + tr[r]] = dd[r];
+        continue;
+      }
       if (v % L == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
       const float cs = __ldg(dS + (int64_t)j * H + tr[r]);
       const float4 as = __ldg(a_src + v), ad = __ldg(a_dst + v);
@@ -879,7 +926,8 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
                                                    const float* __restrict__ s,
                                                    const float* __restrict__ d, float beta,
                                                    float* __restrict__ alpha,
-                                                   uint8_t* __restrict__ mask) {
+                                                   uint8_t* __restrict__ mask,
+                                                   int32_t longest = 0x7fffffff) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
@@ -887,7 +935,7 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
     beg = __ldg(rowptr + i);
     end = __ldg(rowptr + i + 1);
   }
-  const int32_t deg = end - beg;
+  const int32_t deg = end - beg > longest ? 0 : end - beg;  // hub rows: k_gat_attn_long
   const int32_t wdeg = max(deg, __shfl_xor_sync(0xffffffffu, deg, GS));  // warp-uniform
   if (wdeg == 0) return;
   float si[H];
@@ -963,7 +1011,8 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
                                                    const uint8_t* __restrict__ mask,
                                                    const float* __restrict__ da, float beta,
                                                    float* __restrict__ dy,
-                                                   float* __restrict__ dS) {
+                                                   float* __restrict__ dS,
+                                                   int32_t longest = 0x7fffffff) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
@@ -971,10 +1020,11 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     beg = __ldg(rowptr + i);
     end = __ldg(rowptr + i + 1);
   }
-  const int32_t deg = end - beg;
+  const bool hub = end - beg > longest;  // done by k_gat_sbwd_long
+  const int32_t deg = hub ? 0 : end - beg;
   const int32_t wdeg = max(deg, __shfl_xor_sync(0xffffffffu, deg, GS));
   if (wdeg == 0) {
-    if (i < n && gl == 0) {
+    if (i < n && gl == 0 && !hub) {
       float z[H];
 #pragma unroll
       for (int t = 0; t < H; ++t) z[t] = 0.f;
@@ -1015,9 +1065,152 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     }
   }
   group_allreduce<H>(rs, gl, OpSum());
-  if (i < n && gl == 0) st_heads<H>(dS + (int64_t)i * H, rs);
+  if (i < n && gl == 0 && !hub) st_heads<H>(dS + (int64_t)i * H, rs);
 }
 
 static inline unsigned sub_grid(int32_t n) { return (unsigned)((n + 256 / GS - 1) / (256 / GS)); }
+
+// Hub columns of the column pass: sum the segment partials (dM rows and the
+// per-head dD sums) in segment order, then the add_scaled_rows epilogue.
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_col_combine(
+    int32_t nlong, const int32_t* __restrict__ long_col, const int32_t* __restrict__ long_first,
+    const float4* __restrict__ part, const float* __restrict__ ddpart, const float* __restrict__ dS,
+    const float4* __restrict__ a_src, const float4* __restrict__ a_dst, int32_t k,
+    float* __restrict__ dD, float4* __restrict__ dM) {
+  const int lane = threadIdx.x & 31;
+  const int32_t q = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (q >= nlong) return;
+  const int fv = H * k / 4, L = k / 4;
+  const int32_t j = __ldg(long_col + q), s0 = __ldg(long_first + q), s1 = __ldg(long_first + q + 1);
+  for (int v = lane; v < fv; v += 32) {
+    const int t = min(H - 1, v / L);
+    float4 acc = __ldg(part + (int64_t)s0 * fv + v);
+    float dd = __ldg(ddpart + (int64_t)s0 * H + t);
+    for (int32_t sgi = s0 + 1; sgi < s1; ++sgi) {
+      const float4 b = __ldg(part + (int64_t)sgi * fv + v);
+      acc.x += b.x;
+      acc.y += b.y;
+      acc.z += b.z;
+      acc.w += b.w;
+      dd += __ldg(ddpart + (int64_t)sgi * H + t);
+    }
+    if (v % L == 0) dD[(int64_t)j * H + t] = dd;
+    const float cs = __ldg(dS + (int64_t)j * H + t);
+    fma4(acc, cs, __ldg(a_src + v));
+    fma4(acc, dd, __ldg(a_dst + v));
+    dM[(int64_t)j * fv + v] = acc;
+  }
+}
+
+// block-wide reduction of H values (8 warps): every thread gets the totals
+template <int H, class Op>
+__device__ __forceinline__ void block_allreduce(float (&v)[H], float (*sh)[H], Op op) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  allreduce<H>(v, lane, op);
+  if (lane == 0)
+#pragma unroll
+    for (int t = 0; t < H; ++t) sh[w][t] = v[t];
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    float a = sh[0][t];
+    for (int q = 1; q < WPB; ++q) a = op(a, sh[q][t]);
+    v[t] = a;
+  }
+  __syncthreads();
+}
+
+// Hub rows of the attention (kernels.hpp:427-534): one block per row, three
+// strided passes (max, sum of exp, alpha + mask) with block reductions.
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict__ long_row,
+                                                       const int32_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ cols,
+                                                       const float* __restrict__ s,
+                                                       const float* __restrict__ d, float beta,
+                                                       float* __restrict__ alpha,
+                                                       uint8_t* __restrict__ mask) {
+  __shared__ float sh[WPB][H];
+  const int32_t i = __ldg(long_row + blockIdx.x);
+  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  float si[H], mx[H], sm[H];
+  ld_heads<H>(s + (int64_t)i * H, si);
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    mx[t] = -INFINITY;
+    sm[t] = 0.f;
+  }
+  for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    float dj[H];
+    ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+    for (int t = 0; t < H; ++t) mx[t] = fmaxf(mx[t], lrelu(si[t] + dj[t], beta));
+  }
+  block_allreduce<H>(mx, sh, OpMax());
+  for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    float dj[H];
+    ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+#pragma unroll
+    for (int t = 0; t < H; ++t) sm[t] += __expf(lrelu(si[t] + dj[t], beta) - mx[t]);
+  }
+  block_allreduce<H>(sm, sh, OpSum());
+#pragma unroll
+  for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
+  for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    float dj[H], a[H];
+    ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
+    uint32_t pos = 0;
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      const float y = si[t] + dj[t];
+      if (y > 0.f) pos |= 1u << t;
+      a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+    }
+    st_heads<H>(alpha + (int64_t)e * H, a);
+    if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
+  }
+}
+
+// Hub rows of the softmax / LeakyReLU backward and row sums (kernels.hpp:
+// 481-495, 537-588): one block per row, two strided passes.
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict__ long_row,
+                                                       const int32_t* __restrict__ rowptr,
+                                                       const float* __restrict__ alpha,
+                                                       const uint8_t* __restrict__ mask,
+                                                       const float* __restrict__ da, float beta,
+                                                       float* __restrict__ dy,
+                                                       float* __restrict__ dS) {
+  __shared__ float sh[WPB][H];
+  const int32_t i = __ldg(long_row + blockIdx.x);
+  const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
+  float dot[H], rs[H];
+#pragma unroll
+  for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
+  for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    float a[H], g[H];
+    ld_heads<H>(alpha + (int64_t)e * H, a);
+    ld_heads<H>(da + (int64_t)e * H, g);
+#pragma unroll
+    for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
+  }
+  block_allreduce<H>(dot, sh, OpSum());
+  for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    float a[H], g[H], y[H];
+    ld_heads<H>(alpha + (int64_t)e * H, a);
+    ld_heads<H>(da + (int64_t)e * H, g);
+    const uint32_t pos = ld_mask<H>(mask + (int64_t)e * H);
+#pragma unroll
+    for (int t = 0; t < H; ++t) {
+      const float dw = a[t] * (g[t] - dot[t]);
+      y[t] = (pos >> t) & 1u ? dw : beta * dw;
+      rs[t] += y[t];
+    }
+    st_heads<H>(dy + (int64_t)e * H, y);
+  }
+  block_allreduce<H>(rs, sh, OpSum());
+  if (threadIdx.x == 0) st_heads<H>(dS + (int64_t)i * H, rs);
+}
 
 }  // namespace g2

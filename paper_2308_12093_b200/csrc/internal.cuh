@@ -14,11 +14,14 @@ struct LongRows {
   bool built = false;
   const int32_t* rowptr = nullptr;  // the CSR the plan belongs to
   int32_t nseg = 0, nlong = 0;
-  DevBuf seg_beg, seg_end;  // nseg: edge range of every segment
+  DevBuf seg_beg, seg_end, seg_row;  // nseg: edge range and row of every segment
   DevBuf long_row;    // nlong: row id
   DevBuf long_first;  // nlong + 1: first segment of every long row (+ sentinel)
 };
 LongRows& long_rows(sgnn_ctx ctx, LongRows& plan, int32_t n_rows, const int32_t* rowptr);
+// C[long_row[j]] = sum of the segment partials of row j in order (+ bias)
+void spmm_combine(sgnn_ctx ctx, const LongRows& lr, const float* part, int32_t f, float* C,
+                  const float* bias, int32_t ld);
 }  // namespace sgnn
 
 // AdjacencyOp (kernels.hpp:191-211): forward CSR and the CSC arrays that are
@@ -40,6 +43,7 @@ struct sgnn_pattern_s {
   int64_t nnz = 0;
   bool all_self_loops = false;
   sgnn::DevBuf rowptr, cols, colptr, rows, perm, diag;
+  sgnn::LongRows long_rows, long_cols;  // hub-row / hub-column plans
   ~sgnn_pattern_s();
 };
 

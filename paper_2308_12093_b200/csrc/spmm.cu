@@ -328,6 +328,16 @@ __global__ void __launch_bounds__(256) k_spmm_combine(int32_t nlong,
   }
 }
 
+void spmm_combine(sgnn_ctx ctx, const LongRows& lr, const float* part, int32_t f, float* C,
+                  const float* bias, int32_t ld) {
+  if (lr.nlong == 0) return;
+  k_spmm_combine<<<(unsigned)ceil_div(lr.nlong, 8), 256, 0, ctx->stream>>>(
+      lr.nlong, lr.long_row.as<int32_t>(), lr.long_first.as<int32_t>(),
+      reinterpret_cast<const float4*>(part), f / 4, reinterpret_cast<float4*>(C),
+      reinterpret_cast<const float4*>(bias), ld / 4);
+  launched(ctx);
+}
+
 __global__ void k_long_count(int32_t n, const int32_t* __restrict__ rowptr, int32_t seglen,
                              int32_t* __restrict__ segs, int32_t* __restrict__ islong) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
@@ -341,7 +351,8 @@ __global__ void k_long_count(int32_t n, const int32_t* __restrict__ rowptr, int3
 __global__ void k_long_fill(int32_t n, const int32_t* __restrict__ rowptr, int32_t seglen,
                             const int32_t* __restrict__ segoff, const int32_t* __restrict__ longoff,
                             int32_t* __restrict__ seg_beg, int32_t* __restrict__ seg_end,
-                            int32_t* __restrict__ long_row, int32_t* __restrict__ long_first) {
+                            int32_t* __restrict__ seg_row, int32_t* __restrict__ long_row,
+                            int32_t* __restrict__ long_first) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t beg = rowptr[i], end = rowptr[i + 1];
@@ -353,6 +364,7 @@ __global__ void k_long_fill(int32_t n, const int32_t* __restrict__ rowptr, int32
     for (int32_t e = beg; e < end; e += seglen, ++s) {
       seg_beg[s] = e;
       seg_end[s] = min(e + seglen, end);
+      seg_row[s] = (int32_t)i;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) long_first[longoff[n]] = segoff[n];  // sentinel
@@ -389,11 +401,13 @@ LongRows& long_rows(sgnn_ctx ctx, LongRows& plan, int32_t n, const int32_t* rowp
   if (plan.nlong == 0) return plan;
   plan.seg_beg = DevBuf((size_t)plan.nseg * 4, st);
   plan.seg_end = DevBuf((size_t)plan.nseg * 4, st);
+  plan.seg_row = DevBuf((size_t)plan.nseg * 4, st);
   plan.long_row = DevBuf((size_t)plan.nlong * 4, st);
   plan.long_first = DevBuf((size_t)(plan.nlong + 1) * 4, st);
   k_long_fill<<<grid_for(ctx, n, 256), 256, 0, st>>>(n, rowptr, kLongRow, segoff.as<int32_t>(),
                                                      longoff.as<int32_t>(), plan.seg_beg.as<int32_t>(),
                                                      plan.seg_end.as<int32_t>(),
+                                                     plan.seg_row.as<int32_t>(),
                                                      plan.long_row.as<int32_t>(),
                                                      plan.long_first.as<int32_t>());
   launched(ctx);
