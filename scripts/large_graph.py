@@ -1,9 +1,10 @@
 """Config 5 at one GPU: 2-layer GCN / GAT training steps on the large synthetic
-graph (the reference generator synthetic_graph(2,449,029,
-61,859,140/2,449,029, seed 1) is the ER proxy of the 62M-edge graph), 100 input
-features.  Prints one JSON line; results are kept under profiles/.
+graphs, 100 input features: the power-law graph of BASELINE config 5 (device
+Chung-Lu generator, 2,449,029 nodes, 61,859,140 / 2,449,029 average degree,
+exponent 2.5) and the reference generator's uniform ER proxy of SURVEY 8.
+Prints one JSON line; results are kept under profiles/.
 
-  python scripts/large_graph.py [--steps K]
+  python scripts/large_graph.py [--steps K] [--graph powerlaw|uniform|both]
 """
 import argparse
 import json
@@ -25,11 +26,22 @@ N, EDGES, SEED, M_IN = 2449029, 61859140, 1, 100
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--graph", default="both", choices=["powerlaw", "uniform", "both"])
     args = ap.parse_args()
+    kinds = ["powerlaw", "uniform"] if args.graph == "both" else [args.graph]
+    lines = [run(args, kind) for kind in kinds]
+    print(json.dumps({"config5_one_gpu": lines}), flush=True)
+
+
+def run(args, kind):
     ctx = d.Context.default(0)
     stream = torch.cuda.current_stream()
     t0 = time.perf_counter()
-    src, dst = d.synthetic_graph(N, EDGES / N, SEED)
+    if kind == "powerlaw":
+        src, dst = d.powerlaw_graph(N, EDGES / N, 2.5, SEED, ctx)
+        torch.cuda.synchronize()
+    else:
+        src, dst = d.synthetic_graph(N, EDGES / N, SEED)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     A = d.Adjacency.gcn_operator(N, src, dst, torch.float32, "csc", ctx)
@@ -51,10 +63,14 @@ def main():
             ms.append(e0.elapsed_time(e1))
         return statistics.median(ms)
 
-    res = {"workload": "config 5 at 1 GPU: 2-layer train steps (MSE) on the large ER-proxy graph",
-           "graph": f"synthetic_graph(n={N}, deg={EDGES}/{N}, seed={SEED})",
+    maxdeg = int(torch.bincount(src.to(ctx.device).long(), minlength=N).max())
+    res = {"workload": "config 5 at 1 GPU: 2-layer train steps (MSE)",
+           "graph": (f"powerlaw_graph(n={N}, deg={EDGES}/{N}, exponent=2.5, seed={SEED})"
+                     if kind == "powerlaw" else
+                     f"synthetic_graph(n={N}, deg={EDGES}/{N}, seed={SEED}) (ER proxy)"),
+           "max_degree": maxdeg,
            "n": N, "nnz_gcn": A.nnz, "nnz_gat": P.nnz, "m": M_IN,
-           "host_generate_s": round(t_gen, 2), "device_preprocess_s": round(t_pre, 2)}
+           "generate_s": round(t_gen, 2), "device_preprocess_s": round(t_pre, 2)}
     out = {}
     for name, model, graph, ow in (
             ("gcn2", d.Model("gcn2", M_IN, 256, 47, scheme="adaptive", caching=True,
@@ -69,7 +85,10 @@ def main():
     out["gcn2"]["shape"] = f"{M_IN}-256-47 adaptive+caching"
     out["gat2"]["shape"] = f"{M_IN}-(8x32)-(8x8) level full"
     res["steps"] = out
-    print(json.dumps(res), flush=True)
+    print(json.dumps(res), file=sys.stderr, flush=True)
+    del A, P, X
+    torch.cuda.empty_cache()
+    return res
 
 
 if __name__ == "__main__":
