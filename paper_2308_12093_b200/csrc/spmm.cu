@@ -108,7 +108,10 @@ __global__ void __launch_bounds__(256, (R == 1 && sizeof(T) == 4) ? SPMM_MINB : 
                                                   const T* __restrict__ vals,
                                                   const T* __restrict__ B, int32_t f,
                                                   T* __restrict__ C, const T* __restrict__ bias,
-                                                  int32_t ld) {
+                                                  int32_t ld, int32_t longest = 0x7fffffff,
+                                                  const int32_t* __restrict__ seg_beg = nullptr) {
+  // seg_beg != nullptr: rows are hub-row segments [seg_beg[r], rowptr[r]) (rowptr
+  // then carries the segment ends) written to partial rows, see LongRows
   using V = typename VecT<T, W>::type;
   constexpr int RPW = 32 / LPR;  // rows per warp
   const int lane = threadIdx.x & 31;
@@ -125,9 +128,13 @@ __global__ void __launch_bounds__(256, (R == 1 && sizeof(T) == 4) ? SPMM_MINB : 
 
   for (int64_t row0 = warp * RPW; row0 < n_rows; row0 += nwarps * RPW) {
     const int64_t row = row0 + grp;
-    const bool active = row < n_rows;
-    const int32_t beg = active ? rowptr[row] : 0;
-    const int32_t end = active ? rowptr[row + 1] : 0;
+    bool active = row < n_rows;
+    int32_t beg = 0, end = 0;
+    if (active) {
+      beg = seg_beg ? seg_beg[row] : rowptr[row];
+      end = seg_beg ? rowptr[row] : rowptr[row + 1];
+      if (end - beg > longest) active = false, end = beg;  // hub row: segments + combine
+    }
     // column blocks of LPR*R vectors (one pass unless f > 32*R*W)
     for (int cb = 0; cb < fv; cb += LPR * R) {
       T acc[R][W];
@@ -218,7 +225,8 @@ __global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 
                 const int32_t* __restrict__ cols, const float* __restrict__ vals,
                 const float4* __restrict__ B, int32_t fv, float4* __restrict__ C,
                 const float4* __restrict__ bias, int32_t ldv, int32_t longest = 0x7fffffff,
-                const int32_t* __restrict__ seg_beg = nullptr) {
+                const int32_t* __restrict__ seg_beg = nullptr, int32_t ldc = 0) {
+  // ldv: row stride of B (vectors); ldc: row stride of C (0: same as B)
   const int lane = threadIdx.x & 31;
   const int32_t row = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (row >= n_rows) return;
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(256, (R == 1 ? (U <= 2 ? 8 : 6) : (U <= 2 ? 6 
       }
     }
   }
-  float4* dst = C + (uint32_t)row * (uint32_t)ldv + lane;
+  float4* dst = C + (uint32_t)row * (uint32_t)(ldc ? ldc : ldv) + lane;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if ((r == 0 && ok0) || (r == 1 && ok1)) {
@@ -436,8 +444,8 @@ static void launch_lean(sgnn_ctx ctx, int U, int32_t n_rows, const int32_t* rowp
   DevBuf part((size_t)lr->nseg * f * 4, ctx->stream);
   float4* pv = part.as<float4>();
   k_spmm_lean<R, 2, true><<<(unsigned)ceil_div(lr->nseg, 8), 256, 0, ctx->stream>>>(
-      lr->nseg, lr->seg_end.as<int32_t>(), cols, vals, Bv, f / 4, pv, nullptr, f / 4, 0x7fffffff,
-      lr->seg_beg.as<int32_t>());
+      lr->nseg, lr->seg_end.as<int32_t>(), cols, vals, Bv, f / 4, pv, nullptr, ld / 4, 0x7fffffff,
+      lr->seg_beg.as<int32_t>(), f / 4);
   launched(ctx);
   k_spmm_combine<<<(unsigned)ceil_div(lr->nlong, 8), 256, 0, ctx->stream>>>(
       lr->nlong, lr->long_row.as<int32_t>(), lr->long_first.as<int32_t>(), pv, f / 4, Cv, bv,
@@ -448,7 +456,7 @@ static void launch_lean(sgnn_ctx ctx, int U, int32_t n_rows, const int32_t* rowp
 template <class T, int W, int LPR, int U>
 static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, const T* vals, const T* B, int32_t f, T* C,
-                       const T* bias, int32_t ld) {
+                       const T* bias, int32_t ld, int32_t longest, const int32_t* seg_beg) {
   const int rpw = 32 / LPR;
   const int64_t warps = ceil_div(n_rows, rpw);
   const int block = 256;
@@ -460,7 +468,8 @@ static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowpt
 #define CASE(RR)                                                                         \
   case RR:                                                                               \
     k_spmm_csr<T, LPR, RR, W, U><<<(int)grid, block, 0, ctx->stream>>>(n_rows, rowptr, cols, \
-                                                                      vals, B, f, C, bias, ld); \
+                                                                      vals, B, f, C, bias, ld,  \
+                                                                      longest, seg_beg);        \
     break;
     CASE(1) CASE(2) CASE(4) CASE(8)
 #undef CASE
@@ -469,9 +478,29 @@ static void launch_lpr(sgnn_ctx ctx, int R, int32_t n_rows, const int32_t* rowpt
   launched(ctx);
 }
 
+template <class T>
+__global__ void __launch_bounds__(256) k_spmm_combine_t(int32_t nlong,
+                                                        const int32_t* __restrict__ long_row,
+                                                        const int32_t* __restrict__ long_first,
+                                                        const T* __restrict__ part, int32_t f,
+                                                        T* __restrict__ C,
+                                                        const T* __restrict__ bias, int32_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (j >= nlong) return;
+  const int32_t row = long_row[j], s0 = long_first[j], s1 = long_first[j + 1];
+  for (int32_t c = lane; c < f; c += 32) {
+    T a = part[(int64_t)s0 * f + c];
+    for (int32_t sg = s0 + 1; sg < s1; ++sg) a = add_rn(a, part[(int64_t)sg * f + c]);
+    if (bias) a = add_rn(a, bias[c]);
+    C[(int64_t)row * ld + c] = a;
+  }
+}
+
 template <class T, int W>
-static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-                     const T* vals, const T* B, int32_t f, T* C, const T* bias, int32_t ld) {
+static void launch_w1(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
+                      const T* vals, const T* B, int32_t f, T* C, const T* bias, int32_t ld,
+                      int32_t longest, const int32_t* seg_beg) {
   const int fv = f / W;
   int lpr = 1;
   while (lpr < 32 && lpr < fv) lpr <<= 1;
@@ -488,16 +517,35 @@ static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const 
   }
 #define LPR_CASE(L)                                                                             \
   case L:                                                                                       \
-    if (U >= 8) launch_lpr<T, W, L, 8>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld);      \
-    else if (U >= 4) launch_lpr<T, W, L, 4>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld); \
-    else if (U >= 2) launch_lpr<T, W, L, 2>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld); \
-    else launch_lpr<T, W, L, 1>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld);             \
+    if (U >= 8) launch_lpr<T, W, L, 8>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld, longest, seg_beg);      \
+    else if (U >= 4) launch_lpr<T, W, L, 4>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld, longest, seg_beg); \
+    else if (U >= 2) launch_lpr<T, W, L, 2>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld, longest, seg_beg); \
+    else launch_lpr<T, W, L, 1>(ctx, R, n_rows, rowptr, cols, vals, B, f, C, bias, ld, longest, seg_beg);             \
     break;
   switch (lpr) {
     LPR_CASE(1) LPR_CASE(2) LPR_CASE(4) LPR_CASE(8) LPR_CASE(16)
     default: LPR_CASE(32)
   }
 #undef LPR_CASE
+}
+
+// generic path with hub-row splitting: normal rows, then the segments of the
+// long rows into partial rows, then an in-order combine (+ bias)
+template <class T, int W>
+static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
+                     const T* vals, const T* B, int32_t f, T* C, const T* bias, int32_t ld,
+                     const LongRows* lr = nullptr) {
+  const bool split = lr && lr->nlong > 0;
+  launch_w1<T, W>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, ld,
+                  split ? kLongRow : 0x7fffffff, nullptr);
+  if (!split) return;
+  DevBuf part((size_t)lr->nseg * f * sizeof(T), ctx->stream);
+  launch_w1<T, W>(ctx, lr->nseg, lr->seg_end.as<int32_t>(), cols, vals, B, f, part.as<T>(),
+                  nullptr, f, 0x7fffffff, lr->seg_beg.as<int32_t>());
+  k_spmm_combine_t<T><<<(unsigned)ceil_div(lr->nlong, 8), 256, 0, ctx->stream>>>(
+      lr->nlong, lr->long_row.as<int32_t>(), lr->long_first.as<int32_t>(), part.as<T>(), f, C,
+      bias, ld);
+  launched(ctx);
 }
 
 // fp32 rows of 68..256 floats use the lean one-row-per-warp kernel (measured
@@ -535,9 +583,9 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
     }
   }
   if (f % VW == 0 && aligned)
-    launch_w<T, VW>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f);
+    launch_w<T, VW>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f, lr);
   else
-    launch_w<T, 1>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f);
+    launch_w<T, 1>(ctx, n_rows, rowptr, cols, vals, B, f, C, bias, f, lr);
 }
 
 template void spmm_csr<float>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const float*,

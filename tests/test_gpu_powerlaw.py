@@ -84,3 +84,25 @@ def test_layers_on_powerlaw_graph_vs_oracle(orc):
     rg = orc.gat_backward(pat, G2, X, tg, a_s, a_d, h, 0.2, True)
     for a, b in zip((o,) + tuple(g2), (ro,) + tuple(rg)):
         assert orc.max_rel_diff(a.cpu().numpy().astype(np.float64), b) < 1e-4
+
+
+@pytest.mark.parametrize("f", [24, 47, 128, 300])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_spmm_hub_rows_vs_oracle(orc, f, dtype):
+    """Rows longer than the hub threshold run as segments + in-order combine
+    (lean, windowed and generic paths, both directions)."""
+    from paper_2308_12093_b200 import device as d
+
+    n = 3000
+    s, t = d.powerlaw_graph(n, 10.0, 2.1, 5)
+    sh, th = s.cpu().numpy(), t.cpu().numpy()
+    assert np.bincount(sh, minlength=n).max() > 500  # several 128-edge segments
+    op = orc.gcn_operator(n, sh, th)
+    A = d.Adjacency.gcn_operator(n, s, t, dtype, "csc")
+    B = orc.random_uniform(n, f, 9)
+    Bt = torch.from_numpy(B).to("cuda", dtype)
+    ref = orc.spmm_csr(op.rowptr, op.cols, op.vals, B)
+    tol = 1e-5 if dtype == torch.float32 else 1e-13
+    for tr in (False, True):
+        got = A.spmm(Bt, transposed=tr).double().cpu().numpy()
+        assert orc.max_rel_diff(got, ref) < tol, tr  # the operator is symmetric
