@@ -263,6 +263,11 @@ int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache cach
  * with NCCL exchanges (dist.DistGatLayer): column ids index a (gathered)
  * operand of any row count, row ids are block-local, edge values are
  * edge-major (edges x h) in the block's CSR order. */
+/* hub-row plan of a block CSR / CSC (rows longer than 128 edges run as
+ * segments); every block entry point below accepts one (or NULL) */
+typedef struct sgnn_rowplan_s* sgnn_rowplan;
+int sgnn_rowplan_create(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, sgnn_rowplan* out);
+int sgnn_rowplan_destroy(sgnn_rowplan plan);
 /* gemm + node_scores (kernels.hpp:385-423): M = X Theta, s/d per head */
 int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
                        const float* theta, int32_t h, int32_t k, const float* a_src,
@@ -270,24 +275,26 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 /* edge_scores + leaky_relu_edges + edge_softmax (kernels.hpp:427-534) */
 int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, int32_t h, const float* s, const float* d,
-                       double beta, float* alpha, uint8_t* mask);
+                       double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan);
 /* spmm_semibatched + bias (kernels.hpp:219-254) */
 int sgnn_gat_aggregate(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
                        int32_t h, int32_t k, const float* alpha, const float* M,
-                       const float* bias, float* out);
+                       const float* bias, float* out, sgnn_rowplan plan);
 /* sddmm_semibatched (kernels.hpp:342-377) */
 int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-                   int32_t h, int32_t k, const float* M, const float* G, float* da);
+                   int32_t h, int32_t k, const float* M, const float* G, float* da,
+                   sgnn_rowplan plan);
 /* edge_softmax_backward + leaky_relu_edges_backward + edge_row_sums (481-588) */
 int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
                               const float* alpha, const uint8_t* mask, const float* da,
-                              double beta, float* dy, float* dS);
+                              double beta, float* dy, float* dS, sgnn_rowplan plan);
 /* spmm_semibatched_transposed + edge_col_sums + add_scaled_rows (258-295,
  * 614-658) over a block of columns (rows / perm index gathered G / edges) */
 int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
                          const int32_t* rows, const int32_t* perm, int32_t h, int32_t k,
                          const float* G, const float* alpha, const float* dy, const float* dS,
-                         const float* a_src, const float* a_dst, float* dD, float* dM);
+                         const float* a_src, const float* a_dst, float* dD, float* dM,
+                         sgnn_rowplan plan);
 /* column_sums + attention_param_grad (dense.hpp:272-282, kernels.hpp:592-611) */
 int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, const float* G,
                          const float* M, const float* dS, const float* dD, float* d_bias,

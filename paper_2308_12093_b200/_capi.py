@@ -107,12 +107,14 @@ _SIGS = {
     "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
                                  VP, VP]),
     "sgnn_gat_transform": (INT, [VP, VP, I32, I32, VP, I32, I32, VP, VP, VP, VP, VP]),
-    "sgnn_gat_attention": (INT, [VP, I32, VP, VP, I32, VP, VP, D, VP, VP]),
-    "sgnn_gat_aggregate": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP]),
-    "sgnn_gat_sddmm": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP]),
-    "sgnn_gat_softmax_backward": (INT, [VP, I32, VP, I32, VP, VP, VP, D, VP, VP]),
+    "sgnn_rowplan_create": (INT, [VP, I32, VP, PVP]),
+    "sgnn_rowplan_destroy": (INT, [VP]),
+    "sgnn_gat_attention": (INT, [VP, I32, VP, VP, I32, VP, VP, D, VP, VP, VP]),
+    "sgnn_gat_aggregate": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP, VP]),
+    "sgnn_gat_sddmm": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP]),
+    "sgnn_gat_softmax_backward": (INT, [VP, I32, VP, I32, VP, VP, VP, D, VP, VP, VP]),
     "sgnn_gat_column_pass": (INT, [VP, I32, VP, VP, VP, I32, I32, VP, VP, VP, VP, VP, VP, VP,
-                                   VP]),
+                                   VP, VP]),
     "sgnn_gat_param_grads": (INT, [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP]),
     "sgnn_powerlaw_graph_capacity": (I64, [I32, D]),
     "sgnn_powerlaw_graph": (INT, [VP, I32, D, D, U64, VP, VP, PI64]),

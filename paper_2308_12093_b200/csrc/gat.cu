@@ -1189,6 +1189,35 @@ int sgnn_sddmm(sgnn_ctx ctx, sgnn_pattern p, const void* B, int32_t f, const voi
 // interleave them with NCCL exchanges: column ids index a (gathered) operand
 // of any row count, row ids are block-local.  All pointers 16-byte aligned.
 // ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct sgnn_rowplan_s {
+  LongRows plan;
+};
+
+static const LongRows* plan_of(sgnn_rowplan rp) {
+  return rp && rp->plan.nlong > 0 ? &rp->plan : nullptr;
+}
+
+extern "C" {
+
+// hub-row plan of a block CSR (rows longer than 128 edges split into
+// segments), for the block entry points below; NULL plans are allowed there
+int sgnn_rowplan_create(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, sgnn_rowplan* out) {
+  SGNN_API_BEGIN
+  require(ctx && out && (n_rows == 0 || rowptr), "rowplan: null argument");
+  auto* p = new sgnn_rowplan_s;
+  long_rows(ctx, p->plan, n_rows, rowptr);
+  *out = p;
+  SGNN_API_END
+}
+
+int sgnn_rowplan_destroy(sgnn_rowplan p) {
+  SGNN_API_BEGIN
+  delete p;
+  SGNN_API_END
+}
+
 static void block_check(int32_t h, int32_t k) {
   require(v2_R<float>(h, k) != 0, "gat block: needs h in {1,2,4,8}, k % 4 == 0, h*k <= 1024");
 }
@@ -1214,35 +1243,58 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 // d indexed by column id
 int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, int32_t h, const float* s, const float* d,
-                       double beta, float* alpha, uint8_t* mask) {
+                       double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan) {
   SGNN_API_BEGIN
   require(beta > 0, "gat_forward: beta must be positive");
   require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
   if (n_rows == 0) return SGNN_OK;
+  const LongRows* pl = plan_of(plan);
   HR_SWITCH(h, 1, (g2::k_gat_attn4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
-                      n_rows, rowptr, cols, s, d, (float)beta, alpha, mask)));
+                      n_rows, rowptr, cols, s, d, (float)beta, alpha, mask,
+                      pl ? kLongRow : 0x7fffffff)));
   launched(ctx);
+  if (pl) {
+    HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pl->nlong, 256, 0, ctx->stream>>>(
+                        pl->long_row.as<int32_t>(), rowptr, cols, s, d, (float)beta, alpha,
+                        mask)));
+    launched(ctx);
+  }
   SGNN_API_END
 }
 
 // spmm_semibatched + bias (kernels.hpp:219-254): out rows of the block
 int sgnn_gat_aggregate(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
                        int32_t h, int32_t k, const float* alpha, const float* M,
-                       const float* bias, float* out) {
+                       const float* bias, float* out, sgnn_rowplan plan) {
   SGNN_API_BEGIN
   block_check(h, k);
   if (n_rows == 0) return SGNN_OK;
   const int R2 = v2_R<float>(h, k);
-  HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
-                       n_rows, rowptr, cols, alpha, reinterpret_cast<const float4*>(M), k,
-                       reinterpret_cast<const float4*>(bias), reinterpret_cast<float4*>(out))));
+  const LongRows* pl = plan_of(plan);
+  const unsigned wn = v2_windows<float>(h, k);
+  const float4* M4 = reinterpret_cast<const float4*>(M);
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  g2::SegArgs sk;
+  sk.longest = pl ? kLongRow : 0x7fffffff;
+  HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n_rows), wn), 256, 0, ctx->stream>>>(
+                       n_rows, rowptr, cols, alpha, M4, k, b4, o4, sk)));
   launched(ctx);
+  if (pl) {
+    DevBuf part((size_t)pl->nseg * h * k * 4, ctx->stream);
+    HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
+                         pl->nseg, rowptr, cols, alpha, M4, k, b4, o4,
+                         seg_args(*pl, part.as<float>()))));
+    launched(ctx);
+    spmm_combine(ctx, *pl, part.as<float>(), h * k, out, bias, h * k);
+  }
   SGNN_API_END
 }
 
 // sddmm_semibatched (kernels.hpp:342-377): dAlpha edge-major for the block's rows
 int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
-                   int32_t h, int32_t k, const float* M, const float* G, float* da) {
+                   int32_t h, int32_t k, const float* M, const float* G, float* da,
+                   sgnn_rowplan plan) {
   SGNN_API_BEGIN
   block_check(h, k);
   if (n_rows == 0) return SGNN_OK;
@@ -1250,12 +1302,22 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
   const int L = k / 4;
   const float4* M4 = reinterpret_cast<const float4*>(M);
   const float4* G4 = reinterpret_cast<const float4*>(G);
+  const LongRows* pl = plan_of(plan);
+  const unsigned wn = v2_windows<float>(h, k);
+  g2::SegArgs sk;
+  sk.longest = pl ? kLongRow : 0x7fffffff;
   if ((L & (L - 1)) == 0 && L <= 32) {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
-                         n_rows, rowptr, cols, M4, G4, k, da)));
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n_rows), wn), 256, 0, ctx->stream>>>(
+                         n_rows, rowptr, cols, M4, G4, k, da, sk)));
+    if (pl)
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
+                           pl->nseg, rowptr, cols, M4, G4, k, da, seg_args(*pl))));
   } else {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n_rows), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
-                         n_rows, rowptr, cols, M4, G4, k, da)));
+    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n_rows), wn), 256, 0, ctx->stream>>>(
+                         n_rows, rowptr, cols, M4, G4, k, da, sk)));
+    if (pl)
+      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
+                           pl->nseg, rowptr, cols, M4, G4, k, da, seg_args(*pl))));
   }
   launched(ctx);
   SGNN_API_END
@@ -1265,13 +1327,21 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
 // (kernels.hpp:481-495, 537-588)
 int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
                               const float* alpha, const uint8_t* mask, const float* da,
-                              double beta, float* dy, float* dS) {
+                              double beta, float* dy, float* dS, sgnn_rowplan plan) {
   SGNN_API_BEGIN
   require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
   if (n_rows == 0) return SGNN_OK;
+  const LongRows* pl = plan_of(plan);
   HR_SWITCH(h, 1, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
-                      n_rows, rowptr, alpha, mask, da, (float)beta, dy, dS)));
+                      n_rows, rowptr, alpha, mask, da, (float)beta, dy, dS,
+                      pl ? kLongRow : 0x7fffffff)));
   launched(ctx);
+  if (pl) {
+    HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pl->nlong, 256, 0, ctx->stream>>>(
+                        pl->long_row.as<int32_t>(), rowptr, alpha, mask, da, (float)beta, dy,
+                        dS)));
+    launched(ctx);
+  }
   SGNN_API_END
 }
 
@@ -1281,17 +1351,34 @@ int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowpt
 int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
                          const int32_t* rows, const int32_t* perm, int32_t h, int32_t k,
                          const float* G, const float* alpha, const float* dy, const float* dS,
-                         const float* a_src, const float* a_dst, float* dD, float* dM) {
+                         const float* a_src, const float* a_dst, float* dD, float* dM,
+                         sgnn_rowplan plan) {
   SGNN_API_BEGIN
   block_check(h, k);
   if (n_cols == 0) return SGNN_OK;
   const int R2 = v2_R<float>(h, k);
-  HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n_cols), v2_windows<float>(h, k)), 256, 0, ctx->stream>>>(
-                       n_cols, colptr, rows, perm, reinterpret_cast<const float4*>(G), alpha, dy,
-                       dS, reinterpret_cast<const float4*>(a_src),
-                       reinterpret_cast<const float4*>(a_dst), k, dD,
-                       reinterpret_cast<float4*>(dM))));
+  const LongRows* pl = plan_of(plan);
+  const unsigned wn = v2_windows<float>(h, k);
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  const float4* as4 = reinterpret_cast<const float4*>(a_src);
+  const float4* ad4 = reinterpret_cast<const float4*>(a_dst);
+  float4* dM4 = reinterpret_cast<float4*>(dM);
+  g2::SegArgs sk;
+  sk.longest = pl ? kLongRow : 0x7fffffff;
+  HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n_cols), wn), 256, 0, ctx->stream>>>(
+                       n_cols, colptr, rows, perm, G4, alpha, dy, dS, as4, ad4, k, dD, dM4, sk)));
   launched(ctx);
+  if (pl) {
+    DevBuf part((size_t)pl->nseg * h * k * 4, ctx->stream), ddp((size_t)pl->nseg * h * 4, ctx->stream);
+    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
+                         pl->nseg, colptr, rows, perm, G4, alpha, dy, dS, as4, ad4, k, dD, dM4,
+                         seg_args(*pl, part.as<float>(), ddp.as<float>()))));
+    launched(ctx);
+    HR_SWITCH(h, 1, (g2::k_gat_col_combine<HH><<<v2_grid(pl->nlong), 256, 0, ctx->stream>>>(
+                        pl->nlong, pl->long_row.as<int32_t>(), pl->long_first.as<int32_t>(),
+                        part.as<float4>(), ddp.as<float>(), dS, as4, ad4, k, dD, dM4)));
+    launched(ctx);
+  }
   SGNN_API_END
 }
 

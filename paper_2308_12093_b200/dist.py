@@ -17,6 +17,8 @@ and collective logic under gloo.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -392,6 +394,20 @@ class DistGatLayer:
         self.rowptr, self.cols = t(b["rowptr"]), t(b["cols"])
         self.colptr, self.crows, self.perm = t(b["colptr"]), t(b["rows"]), t(b["perm"])
         self.ctx = Context.default(self.dev.index)
+        # hub-row plans of the rank's row and column blocks (power-law graphs)
+        nl = self.r1 - self.r0
+        self.rplan, self.cplan = C.c_void_p(), C.c_void_p()
+        _capi.check(_capi.lib.sgnn_rowplan_create(self.ctx.handle, nl, self.rowptr.data_ptr(),
+                                                  C.byref(self.rplan)))
+        _capi.check(_capi.lib.sgnn_rowplan_create(self.ctx.handle, nl, self.colptr.data_ptr(),
+                                                  C.byref(self.cplan)))
+
+    def __del__(self):
+        lib = self.c.lib if hasattr(self, "c") else None
+        for nm in ("rplan", "cplan"):
+            h = getattr(self, nm, None)
+            if lib is not None and h:
+                lib.sgnn_rowplan_destroy(h)
 
     def _buf(self, slots, width, used, dtype=torch.float32):
         buf = torch.empty((self.world * slots, width), dtype=dtype, device=self.dev)
@@ -423,10 +439,11 @@ class DistGatLayer:
         abuf, amine = self._buf(self.emx, h, self.ne)
         mask = torch.empty((self.ne, h), dtype=torch.uint8, device=self.dev)
         c.check(lib.sgnn_gat_attention(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h,
-                                       P(s_loc), P(dbuf), float(beta), P(amine), P(mask)))
+                                       P(s_loc), P(dbuf), float(beta), P(amine), P(mask),
+                                       self.rplan))
         out = torch.empty((nl, h * k), dtype=torch.float32, device=self.dev)
         c.check(lib.sgnn_gat_aggregate(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h, k,
-                                       P(amine), P(Mbuf), P(bias), P(out)))
+                                       P(amine), P(Mbuf), P(bias), P(out), self.rplan))
         return out, {"X": X_local, "M": Mbuf, "Mmine": Mmine, "alpha": abuf, "amine": amine,
                      "mask": mask, "beta": beta}
 
@@ -441,12 +458,12 @@ class DistGatLayer:
         Gmine.copy_(G_local)
         da = torch.empty((self.ne, h), dtype=torch.float32, device=self.dev)
         c.check(lib.sgnn_gat_sddmm(self.ctx.handle, nl, P(self.rowptr), P(self.cols), h, k,
-                                   P(cache["M"]), P(Gmine), P(da)))
+                                   P(cache["M"]), P(Gmine), P(da), self.rplan))
         dybuf, dymine = self._buf(self.emx, h, self.ne)
         dS = torch.empty((nl, h), dtype=torch.float32, device=self.dev)
         c.check(lib.sgnn_gat_softmax_backward(self.ctx.handle, nl, P(self.rowptr), h,
                                               P(cache["amine"]), P(cache["mask"]), P(da),
-                                              float(beta), P(dymine), P(dS)))
+                                              float(beta), P(dymine), P(dS), self.rplan))
         self._exchange(Gbuf, self.mx)
         self._exchange(cache["alpha"], self.emx)
         self._exchange(dybuf, self.emx)
@@ -454,7 +471,8 @@ class DistGatLayer:
         dM = torch.empty((nl, hk), dtype=torch.float32, device=self.dev)
         c.check(lib.sgnn_gat_column_pass(self.ctx.handle, nl, P(self.colptr), P(self.crows),
                                          P(self.perm), h, k, P(Gbuf), P(cache["alpha"]),
-                                         P(dybuf), P(dS), P(a_src), P(a_dst), P(dD), P(dM)))
+                                         P(dybuf), P(dS), P(a_src), P(a_dst), P(dD), P(dM),
+                                         self.cplan))
         flat = torch.empty(theta.numel() + 3 * hk, dtype=torch.float32, device=self.dev)
         d_theta = flat[:theta.numel()].view_as(theta)
         d_b = flat[theta.numel():theta.numel() + hk]

@@ -174,3 +174,28 @@ def test_dist_gat_layer_world1(nccl_world1, orc, h, k):
         assert torch.equal(a_, b_)
     ref_o = orc.gat_forward(pat, X, *orc.gat_params(m, h, k, 21), h, 0.2)
     assert orc.max_rel_diff(out.double().cpu().numpy(), ref_o) < 1e-4
+
+
+def test_dist_gat_layer_world1_hub_rows(nccl_world1, orc):
+    """The partitioned GAT layer on a power-law graph (hub rows run through the
+    block entry points' row plans): bit-identical to the single-GPU layer."""
+    from paper_2308_12093_b200 import device as d
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m, h, k = 3000, 16, 8, 8
+    s, t = d.powerlaw_graph(n, 10.0, 2.1, 9)
+    P = d.Pattern.gat_pattern(n, s, t)
+    pa = P.arrays()
+    assert int(torch.diff(pa["rowptr"]).max()) > 500
+    layer = pd.DistGatLayer(n, pa["rowptr"].cpu().numpy(), pa["cols"].cpu().numpy(), h, k,
+                            "cuda:0")
+    th, a_s, a_d, b = d.gat_params(m, h, k, 3)
+    X = d.random_uniform(n, m, 1)
+    G = d.random_uniform(n, h * k, 2)
+    out, cache = layer.forward(X, th, a_s, a_d, b)
+    grads = layer.backward(G, th, a_s, a_d, cache, True)
+    o1, c1 = d.gat_forward(P, X, th, a_s, a_d, b, h, 0.2, "full")
+    g1 = d.gat_backward(P, G, th, a_s, a_d, c1, True)
+    assert torch.equal(out, o1)
+    for x, y in zip(grads, g1):
+        assert torch.equal(x, y)
