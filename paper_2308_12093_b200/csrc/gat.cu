@@ -594,20 +594,20 @@ static unsigned v2_windows(int32_t h, int32_t k) {
 // (H, R) -> constexpr instantiation; R <= 32 * H / 32 lanes' worth
 #define HR_SWITCH(H_, R_, ...)                                                        \
   switch (H_ * 16 + R_) {                                                             \
-    case 1 * 16 + 1: { constexpr int HH = 1, RR = 1; __VA_ARGS__; } break;          \
-    case 2 * 16 + 1: { constexpr int HH = 2, RR = 1; __VA_ARGS__; } break;          \
-    case 2 * 16 + 2: { constexpr int HH = 2, RR = 2; __VA_ARGS__; } break;          \
-    case 4 * 16 + 1: { constexpr int HH = 4, RR = 1; __VA_ARGS__; } break;          \
-    case 4 * 16 + 2: { constexpr int HH = 4, RR = 2; __VA_ARGS__; } break;          \
-    case 4 * 16 + 4: { constexpr int HH = 4, RR = 4; __VA_ARGS__; } break;          \
-    case 4 * 16 + 8: { constexpr int HH = 4, RR = 8; __VA_ARGS__; } break;          \
-    case 2 * 16 + 8: { constexpr int HH = 2, RR = 8; __VA_ARGS__; } break;          \
-    case 1 * 16 + 8: { constexpr int HH = 1, RR = 8; __VA_ARGS__; } break;          \
-    case 8 * 16 + 1: { constexpr int HH = 8, RR = 1; __VA_ARGS__; } break;          \
-    case 8 * 16 + 2: { constexpr int HH = 8, RR = 2; __VA_ARGS__; } break;          \
-    case 8 * 16 + 3: { constexpr int HH = 8, RR = 3; __VA_ARGS__; } break;          \
-    case 8 * 16 + 4: { constexpr int HH = 8, RR = 4; __VA_ARGS__; } break;          \
-    case 8 * 16 + 8: { constexpr int HH = 8, RR = 8; __VA_ARGS__; } break;          \
+    case 1 * 16 + 1: { constexpr int HH = 1, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 2 * 16 + 1: { constexpr int HH = 2, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 2 * 16 + 2: { constexpr int HH = 2, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 4 * 16 + 1: { constexpr int HH = 4, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 4 * 16 + 2: { constexpr int HH = 4, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 4 * 16 + 4: { constexpr int HH = 4, RR = 4; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 4 * 16 + 8: { constexpr int HH = 4, RR = 8; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 2 * 16 + 8: { constexpr int HH = 2, RR = 8; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 1 * 16 + 8: { constexpr int HH = 1, RR = 8; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 8 * 16 + 1: { constexpr int HH = 8, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 8 * 16 + 2: { constexpr int HH = 8, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 8 * 16 + 3: { constexpr int HH = 8, RR = 3; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 8 * 16 + 4: { constexpr int HH = 8, RR = 4; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 8 * 16 + 8: { constexpr int HH = 8, RR = 8; (void)HH; (void)RR; __VA_ARGS__; } break;          \
     default: throw invalid_argument("gat: no v2 kernel for this head/width");        \
   }
 

@@ -25,6 +25,12 @@
 namespace g2 {
 
 constexpr int WPB = 8;  // warps (rows) per block
+#ifndef GAT_U2
+#define GAT_U2 2    // dense-row gathers in flight per warp when R <= 2
+#endif
+#ifndef GAT_MINB
+#define GAT_MINB 5  // resident blocks per SM the gather kernels are built for
+#endif
 
 // Hub rows / columns (a LongRows plan, internal.cuh): the row kernels skip rows
 // longer than `longest`; their SEG instantiation runs one warp per segment
@@ -415,11 +421,11 @@ static inline unsigned attn3_grid(int32_t n) {
 // row vectors, U edges in flight; <= 40 registers for 48 resident warps/SM.
 // ---------------------------------------------------------------------------
 template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
                const float4* __restrict__ bias, float4* __restrict__ out, SegArgs sg = {}) {
-  constexpr int U = R >= 4 ? 1 : 2;
+  constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
   const int lane = threadIdx.x & 31;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
@@ -503,11 +509,11 @@ __global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
 // k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
 template <int H, int R, bool P2, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3)
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                  const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
                  float* __restrict__ da, SegArgs sg = {}) {
-  constexpr int U = R >= 4 ? 1 : 2;
+  constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
   __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
@@ -697,13 +703,13 @@ __global__ void __launch_bounds__(256) k_gat_sbwd3(int32_t n, const int32_t* __r
 // identical dD sums, so no reduction is needed.
 // ---------------------------------------------------------------------------
 template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? 5 : 3) k_gat_col2(
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3) k_gat_col2(
     int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
     const int32_t* __restrict__ perm, const float4* __restrict__ G,
     const float* __restrict__ alpha, const float* __restrict__ dy, const float* __restrict__ dS,
     const float4* __restrict__ a_src, const float4* __restrict__ a_dst, int32_t k,
     float* __restrict__ dD, float4* __restrict__ dM, SegArgs sg = {}) {
-  constexpr int U = R >= 4 ? 1 : 2;
+  constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
   const int lane = threadIdx.x & 31;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t j = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
