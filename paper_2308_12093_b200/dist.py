@@ -96,27 +96,6 @@ class DeviceOps:
 
 
 # ---------------------------------------------------------------------------
-# collectives over uneven row blocks
-# ---------------------------------------------------------------------------
-def all_gather_rows(local, bounds, group=None):
-    """Concatenate every rank's row block (padded to the largest block)."""
-    world = len(bounds) - 1
-    sizes = [bounds[p + 1] - bounds[p] for p in range(world)]
-    mx = max(sizes)
-    f = local.shape[1]
-    pad = torch.zeros((mx, f), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
-    buf = torch.empty((world * mx, f), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(buf, pad, group=group)
-    return torch.cat([buf[p * mx: p * mx + sizes[p]] for p in range(world)], 0)
-
-
-def all_reduce_sum(t, group=None):
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t
-
-
-# ---------------------------------------------------------------------------
 # partitioned GCN layer (gcn.hpp:91-193 over row blocks)
 # ---------------------------------------------------------------------------
 def padded_columns(cols, bounds, mx):
