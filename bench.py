@@ -329,7 +329,7 @@ def run_ours(args):
     def sddmm():
         capi.check(capi.lib.sgnn_gat_sddmm(ctx.handle, n, pa["rowptr"].data_ptr(),
                                            pa["cols"].data_ptr(), GAT_H, GAT_K, Mg.data_ptr(),
-                                           Gg.data_ptr(), da.data_ptr()))
+                                           Gg.data_ptr(), da.data_ptr(), None))
 
     sd_ms = statistics.mean(timed(sddmm, reps, 2))
     hk = GAT_H * GAT_K

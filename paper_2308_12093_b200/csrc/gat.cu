@@ -655,7 +655,7 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
   const int R = fast_R<T>(h, k);
   const int R2 = v2_R<T>(h, k);
   const bool v2 = R2 && al16(out) && al16(bias) && al16(a_src) && al16(a_dst);
-  bool scored = false;  // node scores fused into the X.Theta epilogue (k % 32 == 0)
+  bool scored = false;  // node scores fused into the X.Theta epilogue (whole heads per tile)
   if constexpr (sizeof(T) == 4)
     if (v2)
       scored = gemm_scores_f32(ctx, X, n, m, theta, hk, M.as<float>(), a_src, a_dst, h,
@@ -1222,7 +1222,8 @@ static void block_check(int32_t h, int32_t k) {
   require(v2_R<float>(h, k) != 0, "gat block: needs h in {1,2,4,8}, k % 4 == 0, h*k <= 1024");
 }
 
-// node_scores (kernels.hpp:385-423) fused into M = X Theta when k % 32 == 0
+// node_scores (kernels.hpp:385-423) fused into M = X Theta when whole heads fit
+// a GEMM tile (k % 4 == 0, tile width % k == 0)
 int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
                        const float* theta, int32_t h, int32_t k, const float* a_src,
                        const float* a_dst, float* M, float* s, float* d) {

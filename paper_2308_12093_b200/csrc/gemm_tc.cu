@@ -229,7 +229,8 @@ struct Cfg {
 //   warps 6..9  epilogue: TMEM -> registers -> (+bias) -> global, overlapping
 //               the next tile's MMAs
 // EPI: compile-time epilogue extras (the plain GEMM pays nothing for them):
-// bit 0 node scores, bit 1 ReLU + mask out, bit 2 ReLU backward (mask in)
+// bit 0 node scores, bit 1 ReLU + mask out, bit 2 ReLU backward (mask in),
+// bit 3 node scores for head widths k % 32 != 0 (k % 4 == 0)
 template <bool A_MN, bool B_MN, int BN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -495,31 +496,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = m0 + q * 32 + lane;
       float ss = 0.f, sd = 0.f;  // fused node scores of the current head
+      int hrem = sc.k >> 2, head = (EPI & 8) ? n0 / sc.k : 0;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
         if ((EPI & 1) && n0 + c < N) {
           // s[i,t] = sum_c a_src[t,c] M[i,tk+c] (kernels.hpp:385-423): a_src is h x k
-          // row-major, so its flat index is the output column; k % 32 == 0 and
-          // BN % k == 0, so a head is whole within this tile
+          // row-major, so its flat index is the output column; k % 4 == 0 and
+          // BN % k == 0, so a head is whole within this tile and ends on a
+          // float4 boundary (hrem counts the head's float4 groups still to come)
           const int col0 = n0 + c;
           const float4* as4 = reinterpret_cast<const float4*>(sc.a_src + col0);
           const float4* ad4 = reinterpret_cast<const float4*>(sc.a_dst + col0);
+          if (!(EPI & 8)) {  // k % 32 == 0: heads of whole 32-column chunks, one flush per chunk
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // warp-uniform 16-byte loads (L1 broadcast)
-            const float4 as = __ldg(as4 + j), ad = __ldg(ad4 + j);
-            const float m0 = __uint_as_float(r[4 * j]), m1 = __uint_as_float(r[4 * j + 1]);
-            const float m2 = __uint_as_float(r[4 * j + 2]), m3 = __uint_as_float(r[4 * j + 3]);
-            ss = fmaf(m3, as.w, fmaf(m2, as.z, fmaf(m1, as.y, fmaf(m0, as.x, ss))));
-            sd = fmaf(m3, ad.w, fmaf(m2, ad.z, fmaf(m1, ad.y, fmaf(m0, ad.x, sd))));
-          }
-          if ((col0 + 32) % sc.k == 0) {
-            if (row < M) {
-              sc.s[(int64_t)row * sc.h + col0 / sc.k] = ss;
-              sc.d[(int64_t)row * sc.h + col0 / sc.k] = sd;
+            for (int j = 0; j < 8; ++j) {  // warp-uniform 16-byte loads (L1 broadcast)
+              const float4 as = __ldg(as4 + j), ad = __ldg(ad4 + j);
+              const float m0 = __uint_as_float(r[4 * j]), m1 = __uint_as_float(r[4 * j + 1]);
+              const float m2 = __uint_as_float(r[4 * j + 2]), m3 = __uint_as_float(r[4 * j + 3]);
+              ss = fmaf(m3, as.w, fmaf(m2, as.z, fmaf(m1, as.y, fmaf(m0, as.x, ss))));
+              sd = fmaf(m3, ad.w, fmaf(m2, ad.z, fmaf(m1, ad.y, fmaf(m0, ad.x, sd))));
             }
-            ss = sd = 0.f;
+            if ((col0 + 32) % sc.k == 0) {
+              if (row < M) {
+                sc.s[(int64_t)row * sc.h + col0 / sc.k] = ss;
+                sc.d[(int64_t)row * sc.h + col0 / sc.k] = sd;
+              }
+              ss = sd = 0.f;
+            }
+          } else {  // EPI bit 3, k % 4 == 0: a head may end at any float4 of the chunk
+            const int jn = min(8, (N - col0) >> 2);  // float4 groups inside N
+            // all loads first (the flush stores below could alias them, so the
+            // compiler would not hoist them); clamped, so always in bounds --
+            // groups past N only feed a sum that is never stored
+            float4 as[8], ad[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              as[j] = __ldg(as4 + min(j, jn - 1));
+              ad[j] = __ldg(ad4 + min(j, jn - 1));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float m0 = __uint_as_float(r[4 * j]), m1 = __uint_as_float(r[4 * j + 1]);
+              const float m2 = __uint_as_float(r[4 * j + 2]), m3 = __uint_as_float(r[4 * j + 3]);
+              ss = fmaf(m3, as[j].w, fmaf(m2, as[j].z, fmaf(m1, as[j].y, fmaf(m0, as[j].x, ss))));
+              sd = fmaf(m3, ad[j].w, fmaf(m2, ad[j].z, fmaf(m1, ad[j].y, fmaf(m0, ad[j].x, sd))));
+              if (j < jn && --hrem == 0) {
+                if (row < M) {
+                  sc.s[(int64_t)row * sc.h + head] = ss;
+                  sc.d[(int64_t)row * sc.h + head] = sd;
+                }
+                ss = sd = 0.f;
+                hrem = sc.k >> 2;
+                ++head;
+              }
+            }
           }
         }
         if (tma_store) {
@@ -739,9 +771,14 @@ static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& m
   launch<AM, BM_, BN, PR, 0>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc)
   // epilogue extras: only the shapes that use them are instantiated (the
   // caller checked a_mn == false and pre == true)
-  if (sc.a_src) {
+  if (sc.a_src && sc.k % 32 == 0) {
     if (b_mn) launch<false, true, BN, true, 1>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     else launch<false, false, BN, true, 1>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
+  if (sc.a_src) {
+    if (b_mn) launch<false, true, BN, true, 9>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 9>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     return;
   }
   if (sc.relu_out) {
@@ -798,7 +835,11 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
   if ((reinterpret_cast<uintptr_t>(C) & 15) || (bias && (reinterpret_cast<uintptr_t>(bias) & 15)))
     return false;
-  const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
+  // 128 or 160 columns per tile, whichever pads N less (N = 320, the GAT
+  // 8 x 40 slab: two exact 160-wide tiles instead of three 128-wide ones)
+  const int BN = N <= 32 ? 32
+                 : N <= 64 ? 64
+                 : (ceil_div(N, 160) * 160 < ceil_div(N, 128) * 128 ? 160 : 128);
   const bool a_mn = ta, b_mn = !tb;
   // Small B (the parameter matrix Theta): split hi/lo once in global memory so
   // the kernel streams both halves with TMA and spends no smem bandwidth on it.
@@ -828,7 +869,8 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   int splits = 1;
   const int ksteps = (int)ceil_div(K, BK);
   if (tiles < ctx->num_sms && ksteps >= 16) {
-    splits = (int)std::min<int64_t>(ceil_div(ctx->num_sms, tiles), ksteps / 8);
+    // one wave: tiles * splits <= num_sms (a 149th tile would double the time)
+    splits = (int)std::min<int64_t>(ctx->num_sms / tiles, ksteps / 8);
     if (splits < 1) splits = 1;
   }
   const int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
@@ -836,7 +878,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   EpiScores sc;
   if (att_src) {  // fused node scores: whole heads per tile, no split-K, no bias
     const int hk = heads > 0 ? N / heads : 0;
-    if (splits != 1 || bias || heads <= 0 || hk * heads != N || hk % 32 != 0 || BN % hk != 0 ||
+    if (splits != 1 || bias || heads <= 0 || hk * heads != N || hk % 4 != 0 || BN % hk != 0 ||
         (reinterpret_cast<uintptr_t>(att_src) & 15) || (reinterpret_cast<uintptr_t>(att_dst) & 15))
       return false;
     sc.a_src = att_src;
@@ -876,6 +918,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   switch (BN) {
     case 32: dispatch<32>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
     case 64: dispatch<64>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
+    case 160: dispatch<160>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
     default: dispatch<128>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;
   }
   if (splits > 1) {

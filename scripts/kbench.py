@@ -64,6 +64,21 @@ for w in which:
         torch.cuda.synchronize()
         hs = [int(t.view(torch.int32).to(torch.int64).mul(torch.arange(t.numel(), device=dev).view(t.shape) % 1000003 + 1).sum()) for t in (outm, out, o3)]
         print("hash", hs, flush=True); continue
+    elif w.startswith("xform"):  # M = X Theta with the node scores fused: xform32 / xform40
+        from paper_2308_12093_b200 import _capi as capi
+        kk = int(w[5:] or 32); mi = 128 if kk == 32 else 256
+        Xi = torch.randn(n, mi, device=dev); thi = torch.randn(mi, 8 * kk, device=dev)
+        a_s = torch.randn(8 * kk, device=dev); a_d = torch.randn(8 * kk, device=dev)
+        Mo = torch.empty(n, 8 * kk, device=dev); so = torch.empty(n, 8, device=dev); do_ = torch.empty(n, 8, device=dev)
+        ctx = d.Context.default()
+        us = t(lambda: capi.check(capi.lib.sgnn_gat_transform(ctx.handle, Xi.data_ptr(), n, mi, thi.data_ptr(), 8, kk,
+               a_s.data_ptr(), a_d.data_ptr(), Mo.data_ptr(), so.data_ptr(), do_.data_ptr())))
+        byt = 4 * (n * mi + n * 8 * kk)
+    elif w in ("l2nn", "l2tn", "l2nt"):  # Gat2 layer 2: n x 256 <-> n x 320
+        H1 = torch.randn(n, 256, device=dev); Z = torch.randn(n, 320, device=dev); th2 = torch.randn(256, 320, device=dev)
+        f = {"l2nn": lambda: d.gemm(H1, th2), "l2tn": lambda: d.gemm(H1, Z, True, False),
+             "l2nt": lambda: d.gemm(Z, th2, False, True)}[w]
+        us = t(f); byt = 4 * (n * 256 + n * 320)
     elif w == "copy":
         us = t(lambda: out.copy_(G)); byt = 8 * n * k
     print(f"{w}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s", flush=True)

@@ -152,7 +152,10 @@ def test_edge_softmax_requires_self_loops(d):
         d.edge_softmax(p, cu(np.zeros(2)))
 
 
-@pytest.mark.parametrize("shape", [(1000, 7, 5), (300, 128, 256), (4096, 64, 40), (70000, 16, 8)])
+# (20000, 256, 320): 160-wide tiles (two per row block), split-K dTheta shape;
+# (5000, 96, 300): 160-wide tiles with a ragged last tile
+@pytest.mark.parametrize("shape", [(1000, 7, 5), (300, 128, 256), (4096, 64, 40), (70000, 16, 8),
+                                   (20000, 256, 320), (5000, 96, 300)])
 @pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True)])
 def test_gemm_vs_oracle(d, orc, shape, trans):
     n, m, k = shape
@@ -187,3 +190,33 @@ def test_random_uniform_bit_exact(d, golden, orc):
     th, a_s, a_d, b = d.gat_params(9, 3, 5, 23, dtype=torch.float64)
     for got, ref in zip((th, a_s, a_d, b), orc.gat_params(9, 3, 5, 23)):
         assert np.array_equal(np_(got), ref)
+
+
+# fused (per-chunk heads): 8x32; fused (heads ending mid-chunk): 8x40, 8x20,
+# 4x40, 8x16; separate score kernel (heads do not divide the tile): 8x12, 2x40
+@pytest.mark.parametrize("hk", [(8, 32), (8, 40), (8, 20), (4, 40), (8, 16), (8, 12), (2, 40)])
+def test_gat_transform_scores(d, orc, hk):
+    """sgnn_gat_transform: M = X Theta with the node scores (kernels.hpp:385-423)
+    fused into the GEMM epilogue when whole heads fit a tile (k % 4 == 0), else
+    the separate score kernel -- both against float64 numpy."""
+    from paper_2308_12093_b200 import _capi as capi
+    h, k = hk
+    n, m = 9000, 96
+    X = orc.random_uniform(n, m, 3).astype(np.float32)
+    th = orc.random_uniform(m, h * k, 4).astype(np.float32)
+    a_s = orc.random_uniform(h, k, 5).astype(np.float32)
+    a_d = orc.random_uniform(h, k, 6).astype(np.float32)
+    Xc, thc, asc, adc = cu(X), cu(th), cu(a_s), cu(a_d)
+    M = torch.empty((n, h * k), dtype=torch.float32, device="cuda")
+    s = torch.empty((n, h), dtype=torch.float32, device="cuda")
+    dd = torch.empty((n, h), dtype=torch.float32, device="cuda")
+    ctx = d.Context.default()
+    capi.check(capi.lib.sgnn_gat_transform(ctx.handle, Xc.data_ptr(), n, m, thc.data_ptr(), h, k,
+                                           asc.data_ptr(), adc.data_ptr(), M.data_ptr(),
+                                           s.data_ptr(), dd.data_ptr()))
+    Mr = X.astype(np.float64) @ th.astype(np.float64)
+    sr = np.einsum("ntc,tc->nt", Mr.reshape(n, h, k), a_s.astype(np.float64))
+    dr = np.einsum("ntc,tc->nt", Mr.reshape(n, h, k), a_d.astype(np.float64))
+    assert orc.max_rel_diff(np_(M), Mr) < 1e-4
+    assert orc.max_rel_diff(np_(s), sr) < 1e-4
+    assert orc.max_rel_diff(np_(dd), dr) < 1e-4
