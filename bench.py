@@ -168,7 +168,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(r["ms"], 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "weak",
+        "ms_per_step": round(r["ms"], 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config(),
         "cpu_baseline": {"value": round(r["ms"], 3), "unit": "ms", "cores": r["cores"],
