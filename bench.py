@@ -43,7 +43,10 @@ ARXIV_EDGES = 1166243
 SEED = 1
 M_IN, K_OUT = 128, 256
 GAT_H, GAT_K = 8, 32
-GCN2_HID, GAT2_HID, MODEL_OUT = 256, 32, 40  # config 4 (2-layer models, hidden width 256)
+# config 4 (2-layer models, hidden 256): Gcn2 128-256-40; Gat2 hidden 256 per head
+# (the reference's ModelConfig::hidden is per head, model.hpp:128-129):
+# 128-(8x256)-(8x40); the 256-wide total (8x32) variant is reported beside it
+GCN2_HID, GAT2_HID, GAT2_HID_NARROW, MODEL_OUT = 256, 256, 32, 40
 METRIC = "GCN/GAT layer fwd+bwd ms on OGB-Arxiv shape; SpMM/SDDMM HBM GB/s vs peak"
 
 
@@ -126,7 +129,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # reference arm / cpu baseline: the reference's own OpenMP CPU path
 # ---------------------------------------------------------------------------
-def reference_cpu(steps, warmup, kind=0, cores=None):
+def reference_cpu(steps, warmup, kind=0, cores=None, gat2_hid=GAT2_HID):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy  # reference compiled from its unmodified headers (oracle/_ref)
 
@@ -143,8 +146,8 @@ def reference_cpu(steps, warmup, kind=0, cores=None):
     elif kind == 2:  # Gcn2 128-256-40 step, adaptive + caching (config 4)
         h = L.ref_bench_create(2, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GCN2_HID, 1, 0, 0, 1,
                                MODEL_OUT << 8, 2)
-    elif kind == 3:  # Gat2 h=8 128-(8x32)-(8x40) step, level full (config 4)
-        h = L.ref_bench_create(3, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GAT2_HID, GAT_H, 0,
+    elif kind == 3:  # Gat2 h=8 128-(8xhid)-(8x40) step, level full (config 4)
+        h = L.ref_bench_create(3, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, gat2_hid, GAT_H, 0,
                                0, 0, 3 | (MODEL_OUT << 8), 2)
     else:
         h = L.ref_bench_create(1, ARXIV_N, ARXIV_EDGES / ARXIV_N, SEED, M_IN, GAT_K, GAT_H, 1, 0,
@@ -347,17 +350,25 @@ def run_ours(args):
                    seed=SEED + 13, ctx=ctx)
     gat2 = d.Model("gat2", M_IN, GAT2_HID, MODEL_OUT, heads=GAT_H, gat_level="full",
                    seed=SEED + 13, ctx=ctx)
+    gat2n = d.Model("gat2", M_IN, GAT2_HID_NARROW, MODEL_OUT, heads=GAT_H, gat_level="full",
+                    seed=SEED + 13, ctx=ctx)
     t_gcn2 = d.random_uniform(n, MODEL_OUT, SEED + 12, ctx=ctx)
     t_gat2 = d.random_uniform(n, GAT_H * MODEL_OUT, SEED + 12, ctx=ctx)
     gcn2_ms = statistics.mean(timed(d.StepGraph(lambda: gcn2.train_step(A, X, t_gcn2), ctx).replay,
                                     max(3, args.steps), 2))
     gat2_ms = statistics.mean(timed(d.StepGraph(lambda: gat2.train_step(P, X, t_gat2), ctx).replay,
                                     max(3, args.steps), 2))
+    gat2n_ms = statistics.mean(timed(d.StepGraph(lambda: gat2n.train_step(P, X, t_gat2), ctx).replay,
+                                     max(3, args.steps), 2))
+    del gat2, gat2n
     models = {"gcn2": {"ms": round(gcn2_ms, 4), "shape": f"{M_IN}-{GCN2_HID}-{MODEL_OUT}",
                        "relu": True, "caching": True, "scheme": "adaptive"},
               "gat2": {"ms": round(gat2_ms, 4),
                        "shape": f"{M_IN}-({GAT_H}x{GAT2_HID})-({GAT_H}x{MODEL_OUT})",
                        "elu": True, "level": "full"},
+              "gat2_8x32": {"ms": round(gat2n_ms, 4),
+                            "shape": f"{M_IN}-({GAT_H}x{GAT2_HID_NARROW})-({GAT_H}x{MODEL_OUT})",
+                            "elu": True, "level": "full"},
               "loss": "mse vs random_uniform(seed+12)", "input_grad": False}
 
     # ---- e2e through the public API with host buffers -----------------------
@@ -396,9 +407,10 @@ def run_ours(args):
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
         if not args.no_model_cpu:
-            for kind, key in ((2, "gcn2"), (3, "gat2")):
+            for kind, key, hid in ((2, "gcn2", 0), (3, "gat2", GAT2_HID),
+                                   (3, "gat2_8x32", GAT2_HID_NARROW)):
                 try:
-                    r = reference_cpu(1, 0, kind)
+                    r = reference_cpu(1, 0, kind, gat2_hid=hid)
                     models[key]["reference_cpu_ms"] = round(r["ms"], 1)
                     models[key]["reference_cpu_cores"] = r["cores"]
                 except Exception as ex:

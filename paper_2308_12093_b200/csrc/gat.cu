@@ -101,6 +101,44 @@ __global__ void k_node_scores(int32_t n, int32_t h, int32_t k, const T* __restri
   }
 }
 
+// float32 node_scores for head widths the fused / fast paths do not cover
+// (e.g. k = 256): one warp per (node, head), 16-byte loads across the head's
+// k columns (coalesced rows of M, unlike thread-per-(node, head)), xor-tree
+// reduction of the lane partials
+__global__ void __launch_bounds__(256) k_node_scores_warp(int32_t n, int32_t h, int32_t k,
+                                                          const float4* __restrict__ M,
+                                                          const float4* __restrict__ a_src,
+                                                          const float4* __restrict__ a_dst,
+                                                          float* __restrict__ s,
+                                                          float* __restrict__ d) {
+  const int lane = threadIdx.x & 31;
+  const int L = k >> 2;
+  const int64_t total = (int64_t)n * h;
+  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; x < total; x += stride) {
+    const int32_t t = (int32_t)(x % h);
+    const float4* mrow = M + x * L;
+    const float4* as = a_src + (int64_t)t * L;
+    const float4* ad = a_dst + (int64_t)t * L;
+    float sv = 0.f, dv = 0.f;
+#pragma unroll 4
+    for (int c = lane; c < L; c += 32) {
+      const float4 m = __ldg(mrow + c), a = __ldg(as + c), b = __ldg(ad + c);
+      sv = fmaf(m.w, a.w, fmaf(m.z, a.z, fmaf(m.y, a.y, fmaf(m.x, a.x, sv))));
+      dv = fmaf(m.w, b.w, fmaf(m.z, b.z, fmaf(m.y, b.y, fmaf(m.x, b.x, dv))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      dv += __shfl_xor_sync(0xffffffffu, dv, o);
+    }
+    if (lane == 0) {
+      s[x] = sv;
+      d[x] = dv;
+    }
+  }
+}
+
 struct WarpSmem {
   static constexpr int kAlpha = 64;
 };
@@ -513,6 +551,20 @@ static void launch_fwd(sgnn_ctx ctx, int32_t n, const int32_t* rp, const int32_t
 template <class T>
 static void node_scores(sgnn_ctx ctx, int32_t n, int32_t h, int32_t k, const T* M,
                         const T* a_src, const T* a_dst, T* s, T* d) {
+  if constexpr (sizeof(T) == 4) {
+    const bool al = ((reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(a_src) |
+                      reinterpret_cast<uintptr_t>(a_dst)) & 15) == 0;
+    if (k % 4 == 0 && al && n > 0) {
+      const int64_t blocks = ceil_div((int64_t)n * h, 8);
+      const unsigned g = (unsigned)std::min<int64_t>(blocks, (int64_t)ctx->num_sms * 16);
+      k_node_scores_warp<<<g, 256, 0, ctx->stream>>>(
+          n, h, k, reinterpret_cast<const float4*>(M), reinterpret_cast<const float4*>(a_src),
+          reinterpret_cast<const float4*>(a_dst), reinterpret_cast<float*>(s),
+          reinterpret_cast<float*>(d));
+      launched(ctx);
+      return;
+    }
+  }
   k_node_scores<T><<<grid_for(ctx, (int64_t)n * h, 256), 256, 0, ctx->stream>>>(n, h, k, M, a_src,
                                                                                a_dst, s, d);
   launched(ctx);
@@ -591,11 +643,14 @@ static unsigned v2_windows(int32_t h, int32_t k) {
   return (unsigned)((fv + 32 * R - 1) / (32 * R));
 }
 
-// (H, R) -> constexpr instantiation; R <= 32 * H / 32 lanes' worth
+// (H, R) -> constexpr instantiation: every pair v2_R can return
 #define HR_SWITCH(H_, R_, ...)                                                        \
   switch (H_ * 16 + R_) {                                                             \
     case 1 * 16 + 1: { constexpr int HH = 1, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
     case 2 * 16 + 1: { constexpr int HH = 2, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 1 * 16 + 2: { constexpr int HH = 1, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 1 * 16 + 4: { constexpr int HH = 1, RR = 4; (void)HH; (void)RR; __VA_ARGS__; } break;          \
+    case 2 * 16 + 4: { constexpr int HH = 2, RR = 4; (void)HH; (void)RR; __VA_ARGS__; } break;          \
     case 2 * 16 + 2: { constexpr int HH = 2, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
     case 4 * 16 + 1: { constexpr int HH = 4, RR = 1; (void)HH; (void)RR; __VA_ARGS__; } break;          \
     case 4 * 16 + 2: { constexpr int HH = 4, RR = 2; (void)HH; (void)RR; __VA_ARGS__; } break;          \
@@ -612,6 +667,32 @@ static unsigned v2_windows(int32_t h, int32_t k) {
   }
 
 static unsigned v2_grid(int32_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, g2::WPB)); }
+
+// k_gat_sddmm2 reduction mode for head width L = k/4 vectors at R vectors per
+// lane: 1 = power-of-two heads of <= 32 lanes, C in {2,4,8} = heads of C whole
+// 32-lane chunks (R % C == 0), 0 = shared-memory fold (any other width)
+static int sddmm_mode(int L, int R) {
+  if ((L & (L - 1)) == 0 && L <= 32) return 1;
+  const int C = L / 32;
+  if (L % 32 == 0 && (C == 2 || C == 4 || C == 8) && R % C == 0) return C;
+  return 0;
+}
+
+template <int HH, int RR, bool SEGB>
+static void sddmm2_launch(int mode, dim3 grid, cudaStream_t st, int32_t n, const int32_t* rp,
+                          const int32_t* ci, const float4* M4, const float4* G4, int32_t k,
+                          float* da, const g2::SegArgs& sa) {
+#define SDDMM2_GO(PM) g2::k_gat_sddmm2<HH, RR, PM, SEGB><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, da, sa)
+  switch (mode) {
+    case 1: SDDMM2_GO(1); return;
+    case 2: if constexpr (RR % 2 == 0) { SDDMM2_GO(2); return; } break;
+    case 4: if constexpr (RR % 4 == 0) { SDDMM2_GO(4); return; } break;
+    case 8: if constexpr (RR % 8 == 0) { SDDMM2_GO(8); return; } break;
+    default: break;
+  }
+  SDDMM2_GO(0);
+#undef SDDMM2_GO
+}
 
 // hub rows / columns of a pattern (LongRows plan): segment arguments
 static g2::SegArgs seg_args(const LongRows& pl, float* part = nullptr, float* ddpart = nullptr) {
@@ -850,19 +931,12 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const uint8_t* mk = cached ? c->mask.as<uint8_t>() : mask_t.as<uint8_t>();
     const int L = k / 4;
     const unsigned wn = v2_windows<T>(h, k);
-    if ((L & (L - 1)) == 0 && L <= 32) {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
-                           n, rp, ci, M4, G4, k, da.as<float>(), sk)));
-      if (pr.nlong)  // hub rows: per-edge outputs, segments write them directly
-        HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true, true><<<dim3(v2_grid(pr.nseg), wn), 256, 0, st>>>(
-                             pr.nseg, rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
-    } else {
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
-                           n, rp, ci, M4, G4, k, da.as<float>(), sk)));
-      if (pr.nlong)
-        HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false, true><<<dim3(v2_grid(pr.nseg), wn), 256, 0, st>>>(
-                             pr.nseg, rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
-    }
+    const int smode = sddmm_mode(L, R2);
+    HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, false>(smode, dim3(v2_grid(n), wn), st, n, rp, ci, M4,
+                                                   G4, k, da.as<float>(), sk)));
+    if (pr.nlong)  // hub rows: per-edge outputs, segments write them directly
+      HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, true>(smode, dim3(v2_grid(pr.nseg), wn), st, pr.nseg,
+                                                    rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
     launched(ctx);
     HR_SWITCH(h, R2, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
@@ -1307,19 +1381,13 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
   const unsigned wn = v2_windows<float>(h, k);
   g2::SegArgs sk;
   sk.longest = pl ? kLongRow : 0x7fffffff;
-  if ((L & (L - 1)) == 0 && L <= 32) {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true><<<dim3(v2_grid(n_rows), wn), 256, 0, ctx->stream>>>(
-                         n_rows, rowptr, cols, M4, G4, k, da, sk)));
-    if (pl)
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, true, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
-                           pl->nseg, rowptr, cols, M4, G4, k, da, seg_args(*pl))));
-  } else {
-    HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false><<<dim3(v2_grid(n_rows), wn), 256, 0, ctx->stream>>>(
-                         n_rows, rowptr, cols, M4, G4, k, da, sk)));
-    if (pl)
-      HR_SWITCH(h, R2, (g2::k_gat_sddmm2<HH, RR, false, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
-                           pl->nseg, rowptr, cols, M4, G4, k, da, seg_args(*pl))));
-  }
+  const int smode = sddmm_mode(L, R2);
+  HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, false>(smode, dim3(v2_grid(n_rows), wn), ctx->stream,
+                                                 n_rows, rowptr, cols, M4, G4, k, da, sk)));
+  if (pl)
+    HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, true>(smode, dim3(v2_grid(pl->nseg), wn), ctx->stream,
+                                                  pl->nseg, rowptr, cols, M4, G4, k, da,
+                                                  seg_args(*pl))));
   launched(ctx);
   SGNN_API_END
 }

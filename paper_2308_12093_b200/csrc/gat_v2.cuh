@@ -503,18 +503,20 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
 // backward, part 1 (kernels.hpp:342-377 semibatched SDDMM): dAlpha[e, t] =
 // <dX'[i, t, :], M[col_e, t, :]>, edge-major.  Lean warp per row: the row of
 // dX' stays in registers, R 16-byte vectors of M gathered per edge, U edges
-// in flight.  P2 (k/4 a power of two <= 32, heads aligned to lane groups):
-// head-segmented xor reductions over the k/4 lanes of a head; otherwise the
+// in flight.  P2 = 1 (k/4 a power of two <= 32, heads aligned to lane groups):
+// head-segmented xor reductions over the k/4 lanes of a head; P2 = C >= 2
+// (k/4 = 32C, a head spans C whole 32-lane chunks): the chunks are folded in
+// registers and the heads' dots reduce-scattered over the warp; P2 = 0: the
 // per-vector partial dots go through shared memory and H*U lanes fold the
 // k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
-template <int H, int R, bool P2, bool SEG = false>
+template <int H, int R, int P2, bool SEG = false>
 __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                  const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
                  float* __restrict__ da, SegArgs sg = {}) {
   constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
-  __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];
+  __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];  // P2 == 0 only
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     tr[r] = min(H - 1, v / L);
     g[r] = v < fv ? __ldg(G + (int64_t)grow * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const bool lead = P2 && (lane & (L - 1)) == 0;
+  const bool lead = P2 == 1 && (lane & (L - 1)) == 0;
   for (int32_t e = beg; e < end; e += U) {
     uint32_t c[U];
     float4 x[U][R];
@@ -551,7 +553,49 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
         const uint32_t v = vo + r * 32 + lane;
         if (v < (uint32_t)fv) x[u][r] = __ldg(M + c[u] * (uint32_t)fv + v);
       }
-    if (P2 && U * R <= L) {
+    if constexpr (P2 >= 2) {
+      // heads of C = P2 whole chunks: fold chunk partials per head (in chunk
+      // order), then reduce the NV = U * R / C head dots over all 32 lanes by a
+      // reduce-scatter (log2(NV) halving steps, then plain xor steps)
+      constexpr int C = P2, NH = R / C, NV = U * NH;
+      static_assert(R % C == 0 && (NV & (NV - 1)) == 0 && NV <= 32, "wide-head SDDMM shape");
+      float p[NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int qh = 0; qh < NH; ++qh) {
+          float a = 0.f;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int r = qh * C + c;
+            a += vo + r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
+          }
+          p[u * NH + qh] = a;
+        }
+      int off = 16;
+#pragma unroll
+      for (int half = NV / 2; half >= 1; half >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int q = 0; q < half; ++q) {
+          const float send = up ? p[q] : p[q + half];
+          const float keep = up ? p[q + half] : p[q];
+          p[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      for (; off > 0; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
+      int idx = 0;
+      {
+        int o2 = 16;
+#pragma unroll
+        for (int half = NV / 2; half >= 1; half >>= 1, o2 >>= 1)
+          if (lane & o2) idx += half;
+      }
+      const int u = idx / NH, t = vo / L + idx % NH;
+      if ((lane & ((32 / NV) - 1)) == 0 && e + u < end && t < H) da[(int64_t)(e + u) * H + t] = p[0];
+      continue;
+    }
+    if (P2 == 1 && U * R <= L) {
       // transposed reduction: the U*R partial dots of a lane are reduced over
       // the L lanes of its head by a reduce-scatter (each step halves the live
       // values) -- log2(U*R) + ... shuffles instead of U*R*log2(L); lane bits
@@ -593,7 +637,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
       float p[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) p[r] = vo + r * 32 + lane < fv ? dot4(g[r], x[u][r]) : 0.f;
-      if constexpr (P2) {
+      if constexpr (P2 == 1) {
         for (int o = L >> 1; o > 0; o >>= 1)
 #pragma unroll
           for (int r = 0; r < R; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
@@ -607,7 +651,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
           if (vo + r * 32 + lane < fv) sh_p[wib][u][r * 32 + lane] = p[r];
       }
     }
-    if constexpr (!P2) {
+    if constexpr (P2 == 0) {
       __syncwarp();
       const int hw = min(H, (32 * R) / L);  // heads of this window (whole: L | 32R)
       if (lane < U * hw) {

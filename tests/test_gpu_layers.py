@@ -127,7 +127,9 @@ def test_gat_golden_every_level(d, golden, orc):
                                          (400, 7.0, 24, 2, 128), (256, 6.0, 10, 40, 4),
                                          (600, 8.0, 20, 8, 40), (500, 6.0, 12, 4, 12),
                                          (300, 40.0, 16, 2, 20), (700, 5.0, 24, 8, 128),
-                                         (400, 6.0, 16, 8, 256), (300, 9.0, 12, 4, 512)])
+                                         (400, 6.0, 16, 8, 256), (300, 9.0, 12, 4, 512),
+                                         (300, 6.0, 12, 1, 256), (300, 6.0, 12, 2, 256),
+                                         (250, 5.0, 12, 1, 512)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_gat_vs_oracle(d, orc, n, deg, m, h, k, dtype):
     _, s, t = orc.synthetic_graph(n, deg, n + h)

@@ -57,7 +57,7 @@ def test_powerlaw_contract_and_numpy_restatement():
 def test_layers_on_powerlaw_graph_vs_oracle(orc):
     from paper_2308_12093_b200 import device as d
 
-    n, m, k, h, kk = 4000, 24, 40, 8, 8
+    n, m, k = 4000, 24, 40
     s, t = d.powerlaw_graph(n, 12.0, 2.2, 3)
     sh, th = s.cpu().numpy(), t.cpu().numpy()
     assert np.bincount(sh, minlength=n).max() > 300  # rows longer than any fast-path batch
@@ -74,6 +74,19 @@ def test_layers_on_powerlaw_graph_vs_oracle(orc):
         ref = orc.gcn_layer(op, X, theta, bias, (sch.forward, sch.backward, sch.caching), G, True)
         for a, b in zip(got, ref):
             assert orc.max_rel_diff(a.cpu().numpy().astype(np.float64), b) < 1e-4, pol
+
+
+# hub rows on every SDDMM reduction mode: power-of-two heads (8x8), heads of
+# two whole 32-lane chunks (4x256), shared-memory fold (8x40)
+@pytest.mark.parametrize("h,kk", [(8, 8), (4, 256), (8, 40)])
+def test_gat_on_powerlaw_graph_vs_oracle(orc, h, kk):
+    from paper_2308_12093_b200 import device as d
+
+    n, m = 4000, 24
+    s, t = d.powerlaw_graph(n, 12.0, 2.2, 3)
+    sh, th = s.cpu().numpy(), t.cpu().numpy()
+    X = orc.random_uniform(n, m, 11)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()  # noqa: E731
     pat = orc.gat_pattern(n, sh, th)
     P = d.Pattern.gat_pattern(n, s, t)
     tg, a_s, a_d, bg = orc.gat_params(m, h, kk, 21)
