@@ -447,6 +447,9 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     tr[r] = min(H - 1, (vo + r * 32 + lane) / L);
     acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  // 32-lane chunks per head (k/4 = 32C; only the 8-vector wide-slab kernels
+  // test it, the narrow ones keep C = 1 at compile time)
+  const int C = (R == 8 && (L & 31) == 0) ? L >> 5 : 1;
   int32_t e = beg;
   for (; e + U <= end; e += U) {
     uint32_t c[U];
@@ -456,7 +459,8 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
     for (int u = 0; u < U; ++u) {
       c[u] = (uint32_t)__ldg(cols + e + u);
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[u][r] = __ldg(alpha + (int64_t)(e + u) * H + tr[r]);
+      for (int r = 0; r < R; ++r)  // once per head when heads span whole chunks
+        a[u][r] = r % C == 0 ? __ldg(alpha + (int64_t)(e + u) * H + tr[r]) : a[u][r - 1];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -777,6 +781,9 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3) k_gat_col2(
     acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     dd[r] = 0.f;
   }
+  // heads of C whole 32-lane chunks (k/4 = 32C): alpha / dy are loaded once per
+  // head, the other chunks reuse alpha and take the head's dy sum at the end
+  const int C = (R == 8 && (L & 31) == 0) ? L >> 5 : 1;
   int32_t p = beg;
   for (; p + U <= end; p += U) {
     uint32_t row[U];
@@ -793,8 +800,12 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3) k_gat_col2(
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const uint32_t v = vo + r * 32 + lane;
-        a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
-        dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
+        if (r % C == 0) {  // first chunk of its head (every chunk when C == 1)
+          a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
+          dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
+        } else {
+          a[u][r] = a[u][r - 1];
+        }
         if (v < (uint32_t)fv) x[u][r] = __ldg(G + row[u] * (uint32_t)fv + v);
       }
 #pragma unroll
@@ -814,6 +825,9 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3) k_gat_col2(
       if (v < (uint32_t)fv) fma4(acc[r], a, __ldg(G + row * (uint32_t)fv + v));
     }
   }
+#pragma unroll
+  for (int r = 1; r < R; ++r)  // chunks after a head's first take its dy sum
+    if (r % C != 0) dd[r] = dd[r - 1];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int v = vo + r * 32 + lane;
