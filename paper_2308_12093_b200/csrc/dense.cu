@@ -156,7 +156,8 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src = nullptr, const float* att_dst = nullptr,
                  float* s_out = nullptr, float* d_out = nullptr, int heads = 0,
-                 uint8_t* relu_out = nullptr, const uint8_t* mask_in = nullptr);
+                 uint8_t* relu_out = nullptr, const uint8_t* mask_in = nullptr,
+                 const float* elu_saved = nullptr);
 
 // C = op(A) op(B) (+ bias) with ReLU fused into the epilogue: relu_out
 // receives the mask (forward), or mask_in zeroes C where the mask is 0
@@ -166,6 +167,15 @@ bool gemm_relu_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const f
                    uint8_t* relu_out, const uint8_t* mask_in) {
   return gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, nullptr, nullptr, nullptr,
                      nullptr, nullptr, 0, relu_out, mask_in);
+}
+
+// C = op(A) op(B) with the ELU(1) backward fused into the epilogue (mask_in,
+// saved = the activation's forward output); false when it does not apply
+bool gemm_elu_bwd_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                      int32_t rb, int32_t cb, bool ta, bool tb, float* C,
+                      const uint8_t* mask_in, const float* saved) {
+  return gemm_tc_f32(ctx, A, ra, ca, B, rb, cb, ta, tb, C, nullptr, nullptr, nullptr, nullptr,
+                     nullptr, nullptr, 0, nullptr, mask_in, saved);
 }
 
 // M = X Theta with the GAT node scores s, d (n x h) computed in the GEMM

@@ -724,7 +724,8 @@ static void node_scores_fast(sgnn_ctx ctx, int R, int32_t n, int32_t h, int32_t 
 template <class T>
 void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T* theta,
                    const T* a_src, const T* a_dst, const T* bias, int32_t h, int32_t k,
-                   T beta, int level, T* out, sgnn_gat_cache c) {
+                   T beta, int level, T* out, sgnn_gat_cache c, uint8_t* elu_mask = nullptr,
+                   bool* elu_fused = nullptr) {
   const int32_t n = p->n;
   const int64_t q = p->nnz;
   const int32_t hk = h * k;
@@ -767,7 +768,7 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
       ap = alpha_tmp.as<float>();
     }
     const LongRows& pr = long_rows(ctx, p->long_rows, n, rp);
-    const g2::SegArgs sk = skip_long(pr);
+    g2::SegArgs sk = skip_long(pr);
     HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
                          n, rp, ci, sp, dp, (float)beta, ap, mp, sk.longest)));
     launched(ctx);
@@ -775,6 +776,10 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
       HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
                           pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta, ap, mp)));
       launched(ctx);
+    }
+    if (elu_mask && pr.nlong == 0) {  // ELU in the aggregation epilogue (no hub combine)
+      sk.elu_mask = elu_mask;
+      if (elu_fused) *elu_fused = true;
     }
     HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(n, rp, ci, ap, M4, k,
                                                                         b4, o4, sk)));
@@ -886,7 +891,21 @@ static void recompute(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* t
 template <class T>
 void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, const T* a_src,
                     const T* a_dst, sgnn_gat_cache c, bool fg, T* d_theta, T* d_a_src,
-                    T* d_a_dst, T* d_bias, T* d_input) {
+                    T* d_a_dst, T* d_bias, T* d_input, const uint8_t* elu_mask = nullptr,
+                    const T* elu_saved = nullptr, bool* elu_fused = nullptr) {
+  // d_input = dM Theta^T, with the ELU(1) backward of the layer below fused
+  // into the GEMM epilogue when asked for and the tcgen05 path applies
+  auto dx_gemm = [&](const T* dM) {
+    if constexpr (sizeof(T) == 4) {
+      if (elu_mask && elu_saved &&
+          gemm_elu_bwd_f32(ctx, dM, c->n, c->h * c->k, theta, c->m, c->h * c->k, false, true,
+                           d_input, elu_mask, elu_saved)) {
+        if (elu_fused) *elu_fused = true;
+        return;
+      }
+    }
+    gemm<T>(ctx, dM, c->n, c->h * c->k, theta, c->m, c->h * c->k, false, true, d_input);
+  };
   const int32_t n = p->n, h = c->h, k = c->k, hk = h * k, m = c->m;
   const int64_t q = p->nnz;
   const T beta = (T)c->beta;
@@ -989,7 +1008,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     }
     gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
             d_theta);
-    if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+    if (fg) dx_gemm(dM.as<T>());
     return;
   }
   {
@@ -1030,7 +1049,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
       launched(ctx);
       gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
               d_theta);
-      if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+      if (fg) dx_gemm(dM.as<T>());
       return;
     }
   }
@@ -1082,7 +1101,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
   att_grad<T>(ctx, n, h, k, r.Mp, dD.as<T>(), d_a_dst);
   gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
           d_theta);
-  if (fg) gemm<T>(ctx, dM.as<T>(), n, hk, theta, m, hk, false, true, d_input);
+  if (fg) dx_gemm(dM.as<T>());
 }
 
 template <class T>
@@ -1123,6 +1142,27 @@ int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, con
                      const void* a_src, const void* a_dst, const void* bias, int32_t heads,
                      int32_t k, double beta, int level, int dtype, void* out,
                      sgnn_gat_cache* cache) {
+  return sgnn::gat_forward_elu(ctx, p, X, m, theta, a_src, a_dst, bias, heads, k, beta, level,
+                               dtype, out, cache, nullptr, nullptr);
+}
+
+int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
+                      const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
+                      double beta, sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src,
+                      void* d_a_dst, void* d_bias, void* d_input) {
+  (void)beta;  // the forward's beta is kept in the cache
+  return sgnn::gat_backward_elu(ctx, p, d_out, theta, a_src, a_dst, m, heads, k, c, fg, d_theta,
+                                d_a_src, d_a_dst, d_bias, d_input, nullptr, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+int sgnn::gat_forward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m,
+                          const void* theta, const void* a_src, const void* a_dst,
+                          const void* bias, int32_t heads, int32_t k, double beta, int level,
+                          int dtype, void* out, sgnn_gat_cache* cache, uint8_t* elu_mask,
+                          bool* fused) {
+  if (fused) *fused = false;
   SGNN_API_BEGIN
   require(p && p->all_self_loops, "gat_forward: pattern must contain all self loops");
   require(m >= 1 && heads >= 1 && k >= 1, "gat_forward: input width does not match theta");
@@ -1141,7 +1181,7 @@ int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, con
     if (dtype == SGNN_F32)
       gat_forward_t<float>(ctx, p, (const float*)X, m, (const float*)theta, (const float*)a_src,
                            (const float*)a_dst, (const float*)bias, heads, k, (float)beta, level,
-                           (float*)out, c);
+                           (float*)out, c, elu_mask, fused);
     else if (dtype == SGNN_F64)
       gat_forward_t<double>(ctx, p, (const double*)X, m, (const double*)theta,
                             (const double*)a_src, (const double*)a_dst, (const double*)bias,
@@ -1156,10 +1196,12 @@ int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, con
   SGNN_API_END
 }
 
-int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
-                      const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
-                      double beta, sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src,
-                      void* d_a_dst, void* d_bias, void* d_input) {
+int sgnn::gat_backward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
+                           const void* a_src, const void* a_dst, int32_t m, int32_t heads,
+                           int32_t k, sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src,
+                           void* d_a_dst, void* d_bias, void* d_input, const uint8_t* elu_mask,
+                           const void* elu_saved, bool* fused) {
+  if (fused) *fused = false;
   SGNN_API_BEGIN
   require(c != nullptr, "gat_backward: missing saved input");
   require(!c->consumed, "gat_backward: cache already consumed");
@@ -1173,12 +1215,11 @@ int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const voi
     require(c->alpha.get() != nullptr && c->mask.get() != nullptr,
             "gat_backward: cache level promises alpha/mask but they are absent");
   require(!fg || d_input != nullptr, "gat_backward: d_input required for feature gradients");
-  (void)beta;  // the forward's beta is kept in the cache
   if (c->dtype == SGNN_F32)
     gat_backward_t<float>(ctx, p, (const float*)d_out, (const float*)theta,
                           (const float*)a_src, (const float*)a_dst, c, fg != 0,
                           (float*)d_theta, (float*)d_a_src, (float*)d_a_dst, (float*)d_bias,
-                          (float*)d_input);
+                          (float*)d_input, elu_mask, (const float*)elu_saved, fused);
   else
     gat_backward_t<double>(ctx, p, (const double*)d_out, (const double*)theta,
                            (const double*)a_src, (const double*)a_dst, c, fg != 0,
@@ -1186,6 +1227,8 @@ int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const voi
                            (double*)d_bias, (double*)d_input);
   SGNN_API_END
 }
+
+extern "C" {
 
 int sgnn_gat_cache_destroy(sgnn_gat_cache c) {
   SGNN_API_BEGIN

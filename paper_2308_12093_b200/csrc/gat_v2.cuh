@@ -43,6 +43,9 @@ struct SegArgs {
   const int32_t* end = nullptr;
   float4* part = nullptr;  // nseg x fv partial rows
   float* ddpart = nullptr; // nseg x h partial column sums (column pass)
+  // aggregation epilogue: ELU(1) on the output and its byte mask (x > 0),
+  // row-major like the output (dense.hpp:197-228 activation fused)
+  uint8_t* elu_mask = nullptr;
 };
 
 // dense-row gathers in flight per warp: 4 16-byte vectors per lane in total
@@ -498,6 +501,15 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
       o.y += b.y;
       o.z += b.z;
       o.w += b.w;
+      if (sg.elu_mask) {  // same expressions as the separate activation pass
+        const uint32_t mb = (o.x > 0.f ? 1u : 0u) | (o.y > 0.f ? 1u : 0u) << 8 |
+                            (o.z > 0.f ? 1u : 0u) << 16 | (o.w > 0.f ? 1u : 0u) << 24;
+        o.x = o.x > 0.f ? o.x : __fmul_rn(1.f, expf(o.x) - 1.f);
+        o.y = o.y > 0.f ? o.y : __fmul_rn(1.f, expf(o.y) - 1.f);
+        o.z = o.z > 0.f ? o.z : __fmul_rn(1.f, expf(o.z) - 1.f);
+        o.w = o.w > 0.f ? o.w : __fmul_rn(1.f, expf(o.w) - 1.f);
+        reinterpret_cast<uint32_t*>(sg.elu_mask)[(int64_t)i * fv + v] = mb;
+      }
       __stcs(out + (int64_t)i * fv + v, o);
     }
   }

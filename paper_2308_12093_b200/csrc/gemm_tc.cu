@@ -201,6 +201,9 @@ struct EpiScores {
   // mask_in -> out = mask ? out : 0 (the activation's backward)
   uint8_t* relu_out = nullptr;
   const uint8_t* mask_in = nullptr;
+  // ELU(1) backward (dense.hpp:232-268) with mask_in: out = mask ? out :
+  // (saved + 1) * out, saved = the activation's forward output (row-major n x N)
+  const float* elu_saved = nullptr;
 };
 
 template <int BN>
@@ -230,7 +233,8 @@ struct Cfg {
 //               the next tile's MMAs
 // EPI: compile-time epilogue extras (the plain GEMM pays nothing for them):
 // bit 0 node scores, bit 1 ReLU + mask out, bit 2 ReLU backward (mask in),
-// bit 3 node scores for head widths k % 32 != 0 (k % 4 == 0)
+// bit 3 node scores for head widths k % 32 != 0 (k % 4 == 0), bit 4 (with
+// bit 2) ELU backward
 template <bool A_MN, bool B_MN, int BN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -492,14 +496,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int z, m0, n0, kb, nk;
       tile_of(t, z, m0, n0, kb, nk);
       const int abuf = tl & 1;
+      const int row = m0 + q * 32 + lane;
+      // activation-backward inputs of this row's next 32 columns (mask bytes,
+      // saved ELU outputs): fetched one chunk ahead -- the first while the
+      // accumulator is still being produced -- so their latency overlaps the
+      // TMEM loads and stores instead of stalling every chunk
+      constexpr int NSV = (EPI & 16) ? 8 : 1;
+      uint4 mk_n[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      float4 sv_n[NSV];
+      auto fetch = [&](int cc) {
+        const int col = n0 + cc;
+        const bool ok = row < M && col < N;
+        if (EPI & 4) {
+          const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * N + col);
+          mk_n[0] = ok ? __ldg(mp) : make_uint4(0, 0, 0, 0);
+          mk_n[1] = ok ? __ldg(mp + 1) : make_uint4(0, 0, 0, 0);
+        }
+        if (EPI & 16) {
+          const float4* sp = reinterpret_cast<const float4*>(sc.elu_saved + (int64_t)row * N + col);
+#pragma unroll
+          for (int j = 0; j < NSV; ++j) sv_n[j] = ok ? __ldg(sp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      if (EPI & 20) fetch(0);
       mbar_wait(&tfull[abuf], (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = m0 + q * 32 + lane;
       float ss = 0.f, sd = 0.f;  // fused node scores of the current head
       int hrem = sc.k >> 2, head = (EPI & 8) ? n0 / sc.k : 0;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
+        uint4 mk[2];
+        float4 sv[NSV];
+        if (EPI & 20) {
+          mk[0] = mk_n[0];
+          mk[1] = mk_n[1];
+#pragma unroll
+          for (int j = 0; j < NSV; ++j) sv[j] = sv_n[j];
+          if (c + 32 < BN) fetch(c + 32);
+        }
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
         if ((EPI & 1) && n0 + c < N) {
           // s[i,t] = sum_c a_src[t,c] M[i,tk+c] (kernels.hpp:385-423): a_src is h x k
@@ -562,13 +597,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
           const int col0 = n0 + c;
-          uint4 mk[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
           const bool mrow = row < M && col0 < N;  // masks need N % 32 == 0 (host)
-          if ((EPI & 4) && mrow) {
-            const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * N + col0);
-            mk[0] = __ldg(mp);
-            mk[1] = __ldg(mp + 1);
-          }
           uint32_t mo[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -589,12 +618,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z = v.z > 0.f ? v.z : 0.f;
               v.w = v.w > 0.f ? v.w : 0.f;
             }
-            if (EPI & 4) {
+            if ((EPI & 4) && !(EPI & 16)) {
               const uint32_t w = (&mk[j >> 2].x)[j & 3];
               v.x = (w & 0xffu) ? v.x : 0.f;
               v.y = (w & 0xff00u) ? v.y : 0.f;
               v.z = (w & 0xff0000u) ? v.z : 0.f;
               v.w = (w & 0xff000000u) ? v.w : 0.f;
+            }
+            if constexpr ((EPI & 16) != 0) {  // same rounding as the separate pass
+              const uint32_t w = (&mk[j >> 2].x)[j & 3];
+              const float4 e = sv[j];
+              v.x = (w & 0xffu) ? v.x : __fmul_rn(__fadd_rn(e.x, 1.f), v.x);
+              v.y = (w & 0xff00u) ? v.y : __fmul_rn(__fadd_rn(e.y, 1.f), v.y);
+              v.z = (w & 0xff0000u) ? v.z : __fmul_rn(__fadd_rn(e.z, 1.f), v.z);
+              v.w = (w & 0xff000000u) ? v.w : __fmul_rn(__fadd_rn(e.w, 1.f), v.w);
             }
             *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
           }
@@ -786,6 +823,11 @@ static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& m
     else launch<false, false, BN, true, 2>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     return;
   }
+  if (sc.mask_in && sc.elu_saved) {
+    if (b_mn) launch<false, true, BN, true, 20>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 20>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
   if (sc.mask_in) {
     if (b_mn) launch<false, true, BN, true, 4>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     else launch<false, false, BN, true, 4>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
@@ -825,7 +867,8 @@ static bool tc_disabled() {
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src, const float* att_dst, float* s_out,
-                 float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in) {
+                 float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
+                 const float* elu_saved) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
@@ -890,6 +933,8 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   }
   sc.relu_out = relu_out;
   sc.mask_in = mask_in;
+  sc.elu_saved = elu_saved;
+  if (elu_saved && (!mask_in || (reinterpret_cast<uintptr_t>(elu_saved) & 15))) return false;
   if ((sc.a_src || relu_out || mask_in) && (a_mn || !pre)) return false;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
   const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));

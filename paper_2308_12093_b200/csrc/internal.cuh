@@ -97,6 +97,24 @@ bool gemm_relu_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const f
                    int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                    uint8_t* relu_out, const uint8_t* mask_in);
 
+bool gemm_elu_bwd_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                      int32_t rb, int32_t cb, bool ta, bool tb, float* C,
+                      const uint8_t* mask_in, const float* saved);
+
+// GAT layer calls of Gat2 with the ELU(1) fused where the producing kernel
+// allows it: the forward's aggregation epilogue applies ELU to out and writes
+// the mask (*fused = false: out is the plain layer output); the backward's
+// d_input GEMM applies the ELU backward (mask, saved output).  gat.cu.
+int gat_forward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
+                    const void* a_src, const void* a_dst, const void* bias, int32_t heads,
+                    int32_t k, double beta, int level, int dtype, void* out,
+                    sgnn_gat_cache* cache, uint8_t* elu_mask, bool* fused);
+int gat_backward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
+                     const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
+                     sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src, void* d_a_dst,
+                     void* d_bias, void* d_input, const uint8_t* elu_mask,
+                     const void* elu_saved, bool* fused);
+
 // GCN layer calls of the models with ReLU fused where the producing kernel is
 // a tcgen05 GEMM (else a separate activation pass): forward writes the mask
 // and applies ReLU to out; backward applies the ReLU backward (mask_in) to

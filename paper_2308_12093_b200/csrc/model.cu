@@ -112,6 +112,13 @@ void mse(sgnn_ctx ctx, int64_t n, const T* out, const T* target, T* grad, double
   launched(ctx);
 }
 
+// SGNN_NO_ACT_FUSION=1: run the activations as separate passes (tests compare
+// the fused and unfused steps bit for bit); read per call so it can be toggled
+inline bool act_fusion() {
+  const char* e = getenv("SGNN_NO_ACT_FUSION");
+  return !(e && e[0] == '1');
+}
+
 inline void ok(int rc) {
   if (rc == SGNN_OK) return;
   if (rc == SGNN_EINVAL) throw invalid_argument(sgnn_last_error());
@@ -178,18 +185,24 @@ void gat2_step(sgnn_ctx ctx, sgnn_model md, sgnn_pattern P, const T* X, const T*
   if (!out) o2 = DevBuf((size_t)n * w2 * sizeof(T), st);
   T* o = out ? out : o2.as<T>();
   GatCacheGuard c1, c2;
-  ok(sgnn_gat_forward(ctx, P, X, m, prm(0), prm(1), prm(2), prm(3), hd, hid, beta, cf.gat_level,
-                      md->dtype, h.get(), &c1.c));
-  // elu(1) in place: the forward output h is also the saved value elu backward needs
-  act_fwd<T>(ctx, 2, (int64_t)n * w1, h.as<T>(), h.as<T>(), mask.as<uint8_t>());
+  // layer 1 with its ELU(1) fused into the aggregation epilogue when possible,
+  // else applied in place: h is also the saved value the ELU backward needs
+  bool fused = false;
+  ok(gat_forward_elu(ctx, P, X, m, prm(0), prm(1), prm(2), prm(3), hd, hid, beta, cf.gat_level,
+                     md->dtype, h.get(), &c1.c, act_fusion() ? mask.as<uint8_t>() : nullptr,
+                     &fused));
+  if (!fused) act_fwd<T>(ctx, 2, (int64_t)n * w1, h.as<T>(), h.as<T>(), mask.as<uint8_t>());
   ok(sgnn_gat_forward(ctx, P, h.get(), w1, prm(4), prm(5), prm(6), prm(7), hd, k, beta,
                       cf.gat_level, md->dtype, o, &c2.c));
   DevBuf g((size_t)n * w2 * sizeof(T), st), dl(sizeof(double), st);
   mse<T>(ctx, (int64_t)n * w2, o, target, g.as<T>(), loss ? loss : dl.as<double>());
   DevBuf dh((size_t)n * w1 * sizeof(T), st);
-  ok(sgnn_gat_backward(ctx, P, g.get(), prm(4), prm(5), prm(6), w1, hd, k, beta, c2.c, 1,
-                       grads[4], grads[5], grads[6], grads[7], dh.get()));
-  act_bwd<T>(ctx, 2, (int64_t)n * w1, dh.as<T>(), mask.as<uint8_t>(), h.as<T>(), dh.as<T>());
+  // layer 2 backward with the ELU backward fused into its d_input GEMM epilogue
+  ok(gat_backward_elu(ctx, P, g.get(), prm(4), prm(5), prm(6), w1, hd, k, c2.c, 1, grads[4],
+                      grads[5], grads[6], grads[7], dh.get(),
+                      act_fusion() ? mask.as<uint8_t>() : nullptr, h.get(), &fused));
+  if (!fused)
+    act_bwd<T>(ctx, 2, (int64_t)n * w1, dh.as<T>(), mask.as<uint8_t>(), h.as<T>(), dh.as<T>());
   ok(sgnn_gat_backward(ctx, P, dh.get(), prm(0), prm(1), prm(2), m, hd, hid, beta, c1.c,
                        cf.input_grad, grads[0], grads[1], grads[2], grads[3],
                        cf.input_grad ? d_input : nullptr));
