@@ -629,11 +629,21 @@ template <class T>
 static int v2_R(int32_t h, int32_t k) {
   if (sizeof(T) != 4 || getenv("SGNN_GAT_V1")) return 0;
   if (!(h == 1 || h == 2 || h == 4 || h == 8) || k % 4 != 0) return 0;
-  int R = pick_r(h * k / 4);
-  if (h == 8 && R == 4 && h * k / 4 <= 96) R = 3;  // 257..384 wide: 3 vectors per lane
-  if (R <= 8) return R;
-  // wider slabs: 1024-float column windows (gridDim.y), heads whole per window
-  return 256 % (k / 4) == 0 ? 8 : 0;
+  const int fv = h * k / 4, L = k / 4;
+  int R = pick_r(fv);
+  if (h == 8 && R == 4 && fv <= 96) return 3;  // 257..384 wide: 3 vectors per lane
+  // slabs wider than 32 * wr vectors run in column windows (gridDim.y) of
+  // 32 * w vectors, heads whole per window: more warps per row and fewer
+  // registers per lane keep more rows in flight (Arxiv 8 x 256: the three
+  // gather kernels 8.7 ms at w = 8 -> 6.1 ms at w = 2)
+  static const int wr = [] {
+    const char* e = getenv("SGNN_GAT_WIDE_R");  // dev knob: 2 (default), 4, 8
+    return e ? (e[0] == '4' ? 4 : e[0] == '8' ? 8 : 2) : 2;
+  }();
+  if (R > wr)
+    for (int w = wr; w <= 8; w *= 2)
+      if ((32 * w) % L == 0) return w;
+  return R <= 8 ? R : 0;
 }
 
 // column windows of the dense-row gather kernels: slabs wider than 32R vectors

@@ -28,6 +28,9 @@ constexpr int WPB = 8;  // warps (rows) per block
 #ifndef GAT_U2
 #define GAT_U2 2    // dense-row gathers in flight per warp when R <= 2
 #endif
+#ifndef GAT_MINB8
+#define GAT_MINB8 3  // ... at 8 vectors per lane (2 = no spills, but measured slower)
+#endif
 #ifndef GAT_MINB
 #define GAT_MINB 5  // resident blocks per SM the gather kernels are built for
 #endif
@@ -424,7 +427,7 @@ static inline unsigned attn3_grid(int32_t n) {
 // row vectors, U edges in flight; <= 40 registers for 48 resident warps/SM.
 // ---------------------------------------------------------------------------
 template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
     k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
                const float4* __restrict__ bias, float4* __restrict__ out, SegArgs sg = {}) {
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
 // k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
 template <int H, int R, int P2, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3)
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
     k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                  const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
                  float* __restrict__ da, SegArgs sg = {}) {
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd3(int32_t n, const int32_t* __r
 // identical dD sums, so no reduction is needed.
 // ---------------------------------------------------------------------------
 template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : 3) k_gat_col2(
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3)) k_gat_col2(
     int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
     const int32_t* __restrict__ perm, const float4* __restrict__ G,
     const float* __restrict__ alpha, const float* __restrict__ dy, const float* __restrict__ dS,
