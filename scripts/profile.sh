@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round profile capture (run under gpurun): launch list of one bench GCN step,
-# launch list of one GAT layer step, and ncu --set full captures of the top
+# launch list of one GAT layer step, of one Gat2 (config 4, 8x256) model step, and ncu --set full captures of the top
 # kernels of both.  Outputs -> gpurun_out/, summarised by
 # scripts/summarize_profiles.py into profiles/<tag>/.
 set -x
@@ -11,11 +11,14 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ONE=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"k_|gemm|split" --csv --log-file gpurun_out/gat_launches_${TAG}.csv \
     python scripts/kbench.py gat > gpurun_out/gat_launches_${TAG}.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"k_|gemm|split" --csv --log-file gpurun_out/gat2_launches_${TAG}.csv \
+    python scripts/dev/gat2_step.py 256 > gpurun_out/gat2_launches_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_spmm_lean|k_gemm_tc|k_colsum" \
     -s 12 -c 6 -o gpurun_out/full_${TAG} \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-model-cpu > gpurun_out/full_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_gat_attn3|k_gat_agg2|k_gat_sddmm2|k_gat_sbwd3|k_gat_col2|k_node_scores" \
+    -k regex:"k_gat_attn4|k_gat_agg2|k_gat_sddmm2|k_gat_sbwd4|k_gat_col2|k_node_scores" \
     -s 6 -c 6 -o gpurun_out/full_gat_${TAG} \
     python scripts/kbench.py gat > gpurun_out/full_gat_${TAG}.log 2>&1
 ls -la gpurun_out

@@ -67,6 +67,31 @@ def gat_step(ls):
     return ls[a - 2:b - 2] if len(fwd) <= 1 else ls[a - 2:fwd[1] - 2]
 
 
+def gat2_step(ls):
+    """One Gat2 128-(8x256)-(8x40) training step of scripts/dev/gat2_step.py:
+    from the layer-1 Theta split + X.Theta GEMM before a node-score launch to
+    the same point of the next step (the last complete step)."""
+    idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores_warp" in n]
+    if len(idx) < 2:
+        return []
+    return ls[idx[-2] - 2:idx[-1] - 2]
+
+
+def table(title, seg, fname):
+    tot = sum(m.get("gpu__time_duration.sum", 0) for _, m in seg)
+    lines = [title, "", "| kernel | time us | share | DRAM rd MB | DRAM wr MB |",
+             "|---|---|---|---|---|"]
+    with open(os.path.join(DST, fname), "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["kernel", "time_us", "share", "dram_read_MB", "dram_write_MB"])
+        for n, m in seg:
+            t = m.get("gpu__time_duration.sum", 0)
+            rd, wr = m.get("dram__bytes_read.sum", 0) / 1e6, m.get("dram__bytes_write.sum", 0) / 1e6
+            w.writerow([short(n), round(t / 1e3, 2), round(t / tot, 4), round(rd, 2), round(wr, 2)])
+            lines.append(f"| {short(n)} | {t / 1e3:.1f} | {t / tot:.1%} | {rd:.1f} | {wr:.1f} |")
+    return lines + ["", f"step total (serialised): {tot / 1e3:.1f} us", ""]
+
+
 def main():
     ls = launches()
     step = one_step(ls)
@@ -156,6 +181,12 @@ def main():
                 w.writerow([short(n), round(t / 1e3, 2), round(t / gt, 4),
                             round(m.get("dram__bytes_read.sum", 0) / 1e6, 2),
                             round(m.get("dram__bytes_write.sum", 0) / 1e6, 2)])
+    g2path = os.path.join(SRC, f"gat2_launches_{TAG}.csv")
+    if os.path.exists(g2path):
+        seg = gat2_step(launches(f"gat2_launches_{TAG}.csv"))
+        if seg:
+            lines += table("## One Gat2 training step (config 4: Arxiv, 128-(8x256)-(8x40), "
+                           "ELU, MSE, level full)", seg, "gat2_step_launches.csv")
     lines += [
               "## --set full captures (key metrics)", "",
               "(us; DRAM in MB)", "", "| kernel | us | DRAM rd | DRAM wr | DRAM % | L2 % | L1 % | SM % | warps % | tensor pipe % | L2 hit % | regs |",
