@@ -71,7 +71,7 @@ def gat2_step(ls):
     """One Gat2 128-(8x256)-(8x40) training step of scripts/dev/gat2_step.py:
     from the layer-1 Theta split + X.Theta GEMM before a node-score launch to
     the same point of the next step (the last complete step)."""
-    idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores_warp" in n]
+    idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores_warp" in n]  # warp or warp4
     if len(idx) < 2:
         return []
     return ls[idx[-2] - 2:idx[-1] - 2]

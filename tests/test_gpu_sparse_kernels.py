@@ -193,8 +193,10 @@ def test_random_uniform_bit_exact(d, golden, orc):
 
 
 # fused (per-chunk heads): 8x32; fused (heads ending mid-chunk): 8x40, 8x20,
-# 4x40, 8x16; separate score kernel (heads do not divide the tile): 8x12, 2x40
-@pytest.mark.parametrize("hk", [(8, 32), (8, 40), (8, 20), (4, 40), (8, 16), (8, 12), (2, 40)])
+# 4x40, 8x16; separate score kernel (heads do not divide the tile): 8x12, 2x40,
+# and heads wider than a tile (k = 128 LPW, 4 items per warp): 2x256, 8x256, 1x512
+@pytest.mark.parametrize("hk", [(8, 32), (8, 40), (8, 20), (4, 40), (8, 16), (8, 12), (2, 40),
+                                (2, 256), (8, 256), (1, 512)])
 def test_gat_transform_scores(d, orc, hk):
     """sgnn_gat_transform: M = X Theta with the node scores (kernels.hpp:385-423)
     fused into the GEMM epilogue when whole heads fit a tile (k % 4 == 0), else
