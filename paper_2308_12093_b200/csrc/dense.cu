@@ -259,6 +259,26 @@ __global__ void __launch_bounds__(256) k_colsum_final(int32_t nchunks, int32_t c
   }
 }
 
+// out[j] = sum over nchunks partials, one block per column (narrow outputs:
+// a 40-column d_bias took 29 us on two blocks of lane-per-column warps):
+// threads stride the chunk list, then a fixed smem tree (deterministic)
+template <class T>
+__global__ void __launch_bounds__(256) k_colsum_final_col(int32_t nchunks, int32_t cols,
+                                                          const double* __restrict__ part,
+                                                          T* __restrict__ out) {
+  __shared__ double sh[256];
+  const int32_t j = blockIdx.x;
+  double s = 0.0;
+  for (int32_t c = threadIdx.x; c < nchunks; c += 256) s += part[(int64_t)c * cols + j];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = (T)sh[0];
+}
+
 // float rows of cols % 4 == 0 (cols <= 1024): threads own float4 column
 // vectors, 256 / (cols/4) row groups per block stride the chunk, float64
 // accumulation, row groups combined in a fixed order in shared memory.
@@ -329,8 +349,12 @@ void column_sums(sgnn_ctx ctx, const T* X, int32_t rows, int32_t cols, T* out) {
                                                           part.as<double>());
     launched(ctx);
   }
-  k_colsum_final<T><<<(unsigned)ceil_div(cols, 32), 256, 0, ctx->stream>>>(
-      nchunks, cols, part.as<double>(), out);
+  if (cols <= 2 * ctx->num_sms)
+    k_colsum_final_col<T><<<(unsigned)cols, 256, 0, ctx->stream>>>(nchunks, cols,
+                                                                  part.as<double>(), out);
+  else
+    k_colsum_final<T><<<(unsigned)ceil_div(cols, 32), 256, 0, ctx->stream>>>(
+        nchunks, cols, part.as<double>(), out);
   launched(ctx);
 }
 template void column_sums<float>(sgnn_ctx, const float*, int32_t, int32_t, float*);
