@@ -760,6 +760,15 @@ static void sddmm2_launch(int mode, dim3 grid, cudaStream_t st, int32_t n, const
                           const int32_t* ci, const float4* M4, const float4* G4, int32_t k,
                           float* da, const g2::SegArgs& sa) {
 #define SDDMM2_GO(PM) g2::k_gat_sddmm2<HH, RR, PM, SEGB><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, da, sa)
+  // heads of L < 16 vectors, L not a power of two, one window: padded lanes
+  if (mode == 0 && grid.y == 1 && (k / 4) < 16 && HH >= 2) {
+    if ((k / 4) < 8) {
+      g2::k_gat_sddmm_pad<HH, 8, SEGB><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, da, sa);
+    } else {
+      g2::k_gat_sddmm_pad<HH, 16, SEGB><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, da, sa);
+    }
+    return;
+  }
   switch (mode) {
     case 1: SDDMM2_GO(1); return;
     case 2: if constexpr (RR % 2 == 0) { SDDMM2_GO(2); return; } break;

@@ -685,6 +685,84 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 }
 
 // ---------------------------------------------------------------------------
+// SDDMM for head widths L = k/4 that are not a power of two (e.g. k = 40):
+// each head gets LP = 8 or 16 lanes (the next power of two, lanes q >= L
+// idle), so the per-head dots reduce with the transposed xor reduce-scatter
+// of the power-of-two path instead of the shared-memory fold.  One column
+// window (H * LP <= 32 R lanes' worth); U = 2 edges in flight.
+// ---------------------------------------------------------------------------
+template <int H, int LP, bool SEG = false>
+__global__ void __launch_bounds__(256, 3)
+    k_gat_sddmm_pad(int32_t n, const int32_t* __restrict__ rowptr,
+                    const int32_t* __restrict__ cols, const float4* __restrict__ M,
+                    const float4* __restrict__ G, int32_t k, float* __restrict__ da,
+                    SegArgs sg = {}) {
+  constexpr int R = (H * LP + 31) / 32, U = 2, NV = U * R;
+  static_assert(NV <= LP && (NV & (NV - 1)) == 0, "padded SDDMM shape");
+  const int lane = threadIdx.x & 31;
+  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (i >= n) return;
+  const int L = k / 4, fv = H * L;
+  int32_t beg, end, grow = i;
+  if (SEG) {
+    beg = __ldg(sg.beg + i);
+    end = __ldg(sg.end + i);
+    grow = __ldg(sg.row + i);
+  } else {
+    beg = __ldg(rowptr + i);
+    end = __ldg(rowptr + i + 1);
+    if (end - beg > sg.longest) return;
+  }
+  int vv[R];  // vector of slot (r, lane), -1 for a padding lane
+  float4 g[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int slot = r * 32 + lane, t = slot / LP, q = slot % LP;
+    vv[r] = (q < L && t < H) ? t * L + q : -1;
+    g[r] = vv[r] >= 0 ? __ldg(G + (int64_t)grow * fv + vv[r]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // value index a lane holds after the reduce-scatter: bits LP/2 .. LP/NV
+  int idx = 0;
+  {
+    int o2 = LP >> 1;
+#pragma unroll
+    for (int half = NV / 2; half >= 1; half >>= 1, o2 >>= 1)
+      if (lane & o2) idx += half;
+  }
+  const int ou = idx / R, orr = idx % R;
+  const int ot = (orr * 32 + lane) / LP;
+  const bool writer = (lane & ((LP / NV) - 1)) == 0 && ot < H;
+  for (int32_t e = beg; e < end; e += U) {
+    uint32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (uint32_t)__ldg(cols + min(e + u, end - 1));
+    float p[NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float4 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (vv[r] >= 0) x[r] = __ldg(M + c[u] * (uint32_t)fv + vv[r]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) p[u * R + r] = vv[r] >= 0 ? dot4(g[r], x[r]) : 0.f;
+    }
+    int off = LP >> 1;
+#pragma unroll
+    for (int half = NV / 2; half >= 1; half >>= 1, off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int q = 0; q < half; ++q) {
+        const float send = up ? p[q] : p[q + half];
+        const float keep = up ? p[q + half] : p[q];
+        p[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    for (; off > 0; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
+    if (writer && e + ou < end) da[(int64_t)(e + ou) * H + ot] = p[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // backward, part 2 (kernels.hpp:537-567 softmax backward, 481-495 LeakyReLU
 // backward, 571-588 row sums): per row, dot[t] = sum_e alpha dAlpha, dy =
 // mask ? dw : beta dw with dw = alpha (dAlpha - dot), dS[i, t] = sum_e dy.
