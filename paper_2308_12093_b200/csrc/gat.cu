@@ -1087,7 +1087,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
         default: g2::k_grads3_partial<8><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n, k, G4, M4, dS.as<float>(), dD.as<float>(), chunk, part.as<double>()); break;
       }
       launched(ctx);
-      g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(
+      g2::k_grads3_final_col<<<dim3((unsigned)hk, 3), 256, 0, st>>>(
           nb, hk, part.as<double>(), reinterpret_cast<float*>(d_bias),
           reinterpret_cast<float*>(d_a_src), reinterpret_cast<float*>(d_a_dst));
       launched(ctx);
@@ -1607,7 +1607,7 @@ int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, con
     default: g2::k_grads3_partial<8><<<dim3(nb, (unsigned)ceil_div(hk / 4, 256)), 256, 0, st>>>(n_rows, k, G4, M4, dS, dD, chunk, part.as<double>()); break;
   }
   launched(ctx);
-  g2::k_grads3_final<<<dim3((unsigned)ceil_div(hk, 32), 3), 256, 0, st>>>(
+  g2::k_grads3_final_col<<<dim3((unsigned)hk, 3), 256, 0, st>>>(
       nb, hk, part.as<double>(), d_bias, d_a_src, d_a_dst);
   launched(ctx);
   SGNN_API_END

@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 // (dense.hpp:272-282 column_sums for d_bias = 1^T dX'; kernels.hpp:592-611
 // attention_param_grad for d_a_src = sum_i dS[i,t] M[i,t,:] and d_a_dst with
 // dD).  Block partials in float64, threads own 16-byte column vectors, row
-// groups combined in a fixed order; k_grads3_final folds the partials.
+// groups combined in a fixed order; k_grads3_final_col folds the partials.
 // part layout: [block][3][hk] (db | d_a_src | d_a_dst, the latter h x k).
 // ---------------------------------------------------------------------------
 template <int H>
@@ -1004,37 +1004,29 @@ __global__ void __launch_bounds__(256) k_grads3_partial(int32_t n, int32_t k,
   }
 }
 
-// out[q][c] = sum over blocks of part[b][q][c]; blockIdx.y = q, 32 columns per
-// block, 8 warps x 4 independent chains, fixed-order combine.
-__global__ void __launch_bounds__(256) k_grads3_final(int32_t nb, int32_t hk,
-                                                      const double* __restrict__ part,
-                                                      float* __restrict__ db,
-                                                      float* __restrict__ das,
-                                                      float* __restrict__ dad) {
-  __shared__ double sh[8][33];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = blockIdx.y;
-  const int32_t c = blockIdx.x * 32 + l;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  if (c < hk) {
-    const double* p = part + (int64_t)q * hk + c;
-    const int64_t st = 3LL * hk;
-    int32_t b = w;
-    for (; b + 24 < nb; b += 32) {
-      s0 += p[b * st];
-      s1 += p[(b + 8) * st];
-      s2 += p[(b + 16) * st];
-      s3 += p[(b + 24) * st];
-    }
-    for (; b < nb; b += 8) s0 += p[b * st];
-  }
-  sh[w][l] = (s0 + s1) + (s2 + s3);
+// out[q][c] = sum over blocks of part[b][q][c], one block per output column
+// (grid hk x 3): threads stride the nb partials, then a fixed smem tree -- a
+// few L2 round trips instead of nb / 32 dependent ones per lane (hk = 256:
+// 18 -> 6 us)
+__global__ void __launch_bounds__(256) k_grads3_final_col(int32_t nb, int32_t hk,
+                                                          const double* __restrict__ part,
+                                                          float* __restrict__ db,
+                                                          float* __restrict__ das,
+                                                          float* __restrict__ dad) {
+  __shared__ double sh[256];
+  const int32_t c = blockIdx.x;
+  const int q = blockIdx.y;
+  const int64_t st = 3LL * hk;
+  const double* p = part + (int64_t)q * hk + c;
+  double s = 0.0;
+  for (int32_t b = threadIdx.x; b < nb; b += 256) s += p[b * st];
+  sh[threadIdx.x] = s;
   __syncthreads();
-  if (w == 0 && c < hk) {
-    double t = 0.0;
-#pragma unroll
-    for (int z = 0; z < 8; ++z) t += sh[z][l];
-    (q == 0 ? db : q == 1 ? das : dad)[c] = (float)t;
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) (q == 0 ? db : q == 1 ? das : dad)[c] = (float)sh[0];
 }
 
 // ---------------------------------------------------------------------------
