@@ -715,34 +715,23 @@ __global__ void __launch_bounds__(256) k_reduce_splits(int splits, int64_t MN, i
   }
 }
 
-// out[n] = sum over (z, warp) of the converters' column-sum partials: a block
-// owns 32 columns, its 8 warps fold every 8th partial with 4 independent
-// chains, then a fixed-order smem combine (deterministic)
+// out[n] = sum over (z, warp) of the converters' column-sum partials: one
+// block per column, threads stride the partials, then a fixed-order smem tree
+// (deterministic; a few L2 round trips instead of parts / 32 dependent ones)
 __global__ void __launch_bounds__(256) k_colsum_parts(int parts, int N,
                                                       const float* __restrict__ cs_part,
                                                       float* __restrict__ out) {
-  __shared__ double sh[8][33];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int n = blockIdx.x * 32 + l;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  if (n < N) {
-    int p = w;
-    for (; p + 24 < parts; p += 32) {
-      s0 += (double)cs_part[(int64_t)p * N + n];
-      s1 += (double)cs_part[(int64_t)(p + 8) * N + n];
-      s2 += (double)cs_part[(int64_t)(p + 16) * N + n];
-      s3 += (double)cs_part[(int64_t)(p + 24) * N + n];
-    }
-    for (; p < parts; p += 8) s0 += (double)cs_part[(int64_t)p * N + n];
-  }
-  sh[w][l] = (s0 + s1) + (s2 + s3);
+  __shared__ double sh[256];
+  const int n = blockIdx.x;
+  double s = 0.0;
+  for (int p = threadIdx.x; p < parts; p += 256) s += (double)cs_part[(int64_t)p * N + n];
+  sh[threadIdx.x] = s;
   __syncthreads();
-  if (w == 0 && n < N) {
-    double t = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sh[k][l];
-    out[n] = (float)t;
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[n] = (float)sh[0];
 }
 
 // ---- host side -------------------------------------------------------------
@@ -973,8 +962,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     launched(ctx);
   }
   if (colsum_b) {
-    k_colsum_parts<<<(unsigned)ceil_div(N, 32), 256, 0, ctx->stream>>>(splits * 4, N, cs,
-                                                                        colsum_b);
+    k_colsum_parts<<<(unsigned)N, 256, 0, ctx->stream>>>(splits * 4, N, cs, colsum_b);
     launched(ctx);
   }
   return true;
