@@ -704,8 +704,8 @@ static int v2_R(int32_t h, int32_t k) {
   // registers per lane keep more rows in flight (Arxiv 8 x 256: the three
   // gather kernels 8.7 ms at w = 8 -> 6.1 ms at w = 2)
   static const int wr = [] {
-    const char* e = getenv("SGNN_GAT_WIDE_R");  // dev knob: 2 (default), 4, 8
-    return e ? (e[0] == '4' ? 4 : e[0] == '8' ? 8 : 2) : 2;
+    const char* e = getenv("SGNN_GAT_WIDE_R");  // dev knob: 1, 2 (default), 4, 8
+    return e ? (e[0] == '1' ? 1 : e[0] == '4' ? 4 : e[0] == '8' ? 8 : 2) : 2;
   }();
   if (R > wr)
     for (int w = wr; w <= 8; w *= 2)
