@@ -218,7 +218,7 @@ __device__ __forceinline__ void row_stats(int lane, int32_t beg, int32_t end,
   const bool single = end - beg <= 32;
 #pragma unroll
   for (int t = 0; t < H; ++t) {
-    e[t] = (single && beg + lane < end) ? __expf(w[t] - mx[t]) : 0.f;
+    e[t] = (single && beg + lane < end) ? expf(w[t] - mx[t]) : 0.f;
     sm[t] = e[t];
   }
   if (!single) {
@@ -228,7 +228,7 @@ __device__ __forceinline__ void row_stats(int lane, int32_t beg, int32_t end,
         float dj[H];
         ld_heads<H>(d + (int64_t)__ldg(cols + ee) * H, dj);
 #pragma unroll
-        for (int t = 0; t < H; ++t) sm[t] += __expf(lrelu(si[t] + dj[t], beta) - mx[t]);
+        for (int t = 0; t < H; ++t) sm[t] += expf(lrelu(si[t] + dj[t], beta) - mx[t]);
       }
     }
   }
@@ -250,7 +250,7 @@ __device__ __forceinline__ void edge_alpha(int32_t ee, const int32_t* __restrict
   for (int t = 0; t < H; ++t) {
     const float y = si[t] + dj[t];
     if (y > 0.f) pos |= 1u << t;
-    a[t] = __expf(lrelu(y, beta) - mx[t]) * inv[t];
+    a[t] = expf(lrelu(y, beta) - mx[t]) * inv[t];
   }
 }
 
@@ -327,7 +327,7 @@ __device__ __forceinline__ uint32_t restage_alpha(int32_t ee, const int32_t* __r
   for (int t = 0; t < H; ++t) {
     const float y = st[0][t] + dj[t];
     if (y > 0.f) pos |= 1u << t;
-    a[t] = __expf(lrelu(y, beta) - st[1][t]) * st[2][t];
+    a[t] = expf(lrelu(y, beta) - st[1][t]) * st[2][t];
   }
   return pos;
 }
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(256) k_gat_attn3(int32_t n, const int32_t* __r
       for (int t = 0; t < H; ++t) {
         const float w = lrelu(si[t] + dj[t], beta);
         const float mn = fmaxf(mx[t], w);
-        sm[t] = sm[t] * __expf(mx[t] - mn) + __expf(w - mn);
+        sm[t] = sm[t] * expf(mx[t] - mn) + expf(w - mn);
         mx[t] = mn;
       }
     }
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256) k_gat_attn3(int32_t n, const int32_t* __r
       for (int t = 0; t < H; ++t) {
         const float y = si[t] + dj[t];
         if (y > 0.f) pos |= 1u << t;
-        a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+        a[t] = expf(lrelu(y, beta) - mx[t]) * sm[t];
       }
       st_heads<H>(alpha + (int64_t)e * H, a);
       if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
         for (int t = 0; t < H; ++t) w[t] = lrelu(si[t] + dj[t], beta);
       }
 #pragma unroll
-      for (int t = 0; t < H; ++t) sm[t] += __expf(w[t] - mx[t]);
+      for (int t = 0; t < H; ++t) sm[t] += expf(w[t] - mx[t]);
     }
   }
   group_allreduce<H>(sm, gl, OpSum());
@@ -1136,7 +1136,7 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
       uint32_t pos = pos1;
       if (one) {  // scores still in registers: no second gather
 #pragma unroll
-        for (int t = 0; t < H; ++t) a[t] = __expf(w[t] - mx[t]) * sm[t];
+        for (int t = 0; t < H; ++t) a[t] = expf(w[t] - mx[t]) * sm[t];
       } else {
         float dj[H];
         pos = 0;
@@ -1145,7 +1145,7 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
         for (int t = 0; t < H; ++t) {
           const float y = si[t] + dj[t];
           if (y > 0.f) pos |= 1u << t;
-          a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+          a[t] = expf(lrelu(y, beta) - mx[t]) * sm[t];
         }
       }
       st_heads<H>(alpha + (int64_t)e * H, a);
@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict
     float dj[H];
     ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
 #pragma unroll
-    for (int t = 0; t < H; ++t) sm[t] += __expf(lrelu(si[t] + dj[t], beta) - mx[t]);
+    for (int t = 0; t < H; ++t) sm[t] += expf(lrelu(si[t] + dj[t], beta) - mx[t]);
   }
   block_allreduce<H>(sm, sh, OpSum());
 #pragma unroll
@@ -1314,7 +1314,7 @@ __global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict
     for (int t = 0; t < H; ++t) {
       const float y = si[t] + dj[t];
       if (y > 0.f) pos |= 1u << t;
-      a[t] = __expf(lrelu(y, beta) - mx[t]) * sm[t];
+      a[t] = expf(lrelu(y, beta) - mx[t]) * sm[t];
     }
     st_heads<H>(alpha + (int64_t)e * H, a);
     if (mask) st_mask<H>(mask + (int64_t)e * H, pos);

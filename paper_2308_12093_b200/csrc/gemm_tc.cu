@@ -134,6 +134,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -204,6 +212,12 @@ struct EpiScores {
   // ELU(1) backward (dense.hpp:232-268) with mask_in: out = mask ? out :
   // (saved + 1) * out, saved = the activation's forward output (row-major n x N)
   const float* elu_saved = nullptr;
+  // k-block drain mode (K > 256, BN <= 128): every k-block is accumulated
+  // afresh in one of three TMEM accumulators and added into fp32 registers
+  // by the epilogue (round-to-nearest), instead of ~12 truncating tensor-core
+  // accumulations per k-block into one growing sum (5e-6 relative bias at
+  // K = 500, measured); the final sum goes back to TMEM for the epilogue
+  bool drain = false;
 };
 
 template <int BN>
@@ -215,7 +229,10 @@ struct Cfg {
   static constexpr int EPI_BYTES = 4 * 2 * 4096;  // 4 epilogue warps x 2 x (32 x 32 fp32)
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int NA = 2;                                // TMEM A buffers (hi|lo, 64 cols)
-  static constexpr uint32_t USED = 2 * BN + NA * 64;          // accumulators + A buffers
+  // accumulators: 3 when BN <= 128 (the k-block drain mode rotates three),
+  // else 2 (the tile double buffer)
+  static constexpr int NACC = BN <= 128 ? 3 : 2;
+  static constexpr uint32_t USED = NACC * BN + NA * 64;       // accumulators + A buffers
   static constexpr uint32_t TMEM_COLS = USED <= 256 ? 256 : 512;
 };
 
@@ -241,7 +258,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
               int M, int N, int K, int kchunk, int splits, float* __restrict__ C, int ldc,
               const float* __restrict__ bias, float* __restrict__ part, int tma_store,
-              float* __restrict__ cs_part, const EpiScores sc) {
+              double* __restrict__ cs_part, const EpiScores sc) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
   constexpr int NA = CF::NA;
@@ -253,9 +270,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + S;
   uint64_t* afull = empty + S;    // [NA] converters -> MMA
   uint64_t* aempty = afull + NA;  // [NA] MMA -> converters
-  uint64_t* tfull = aempty + NA;  // [2]
-  uint64_t* tempty = tfull + 2;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = aempty + NA;  // [3]
+  uint64_t* tempty = tfull + 3;   // [3]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
@@ -285,7 +302,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&afull[a], 4);
       mbar_init(&aempty[a], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 3; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_a = tmem + 2 * BN;  // A buffers after the two accumulators
+  const uint32_t tmem_a = tmem + CF::NACC * BN;  // A buffers after the accumulators
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -342,15 +359,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc(BN, false, B_MN);  // A from TMEM is K-major
-      int it = 0, tl = 0;
+      int it = 0, tl = 0, dr = 0;
+      const bool kdrain = sc.drain;  // per-k-block accumulators (three)
+      const int nacc = 3;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
         int z, m0, n0, kb, nk;
         tile_of(t, z, m0, n0, kb, nk);
-        const int abuf = tl & 1;
-        mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tacc = tmem + (uint32_t)(abuf * BN);
+        int abuf = tl & 1;
+        uint32_t tacc = tmem + (uint32_t)(abuf * BN);
+        if (!kdrain) {
+          mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
         for (int ks = 0; ks < nk; ++ks, ++it) {
+          if (kdrain) {  // every k-block accumulates afresh into the next accumulator
+            abuf = dr % nacc;
+            tacc = tmem + (uint32_t)(abuf * BN);
+            mbar_wait(&tempty[abuf], ((dr / nacc) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
           const int s = it % S, a = it % NA;
           mbar_wait(&afull[a], (it / NA) & 1);  // implies full[s] (converters waited on it)
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -364,15 +391,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
             const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
             const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
-            const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t acc = ((ks > 0 && !kdrain) || kk > 0) ? 1u : 0u;
             mma_tf32_ts(tacc, ta + kk * 8, dbh, idesc, acc);       // hi . hi
             mma_tf32_ts(tacc, ta + kk * 8, dbl, idesc, 1u);        // hi . lo
             mma_tf32_ts(tacc, ta + 32 + kk * 8, dbh, idesc, 1u);   // lo . hi
           }
           umma_commit(&empty[s]);   // smem stage free
           umma_commit(&aempty[a]);  // TMEM A buffer free
+          if (kdrain) {
+            umma_commit(&tfull[abuf]);  // this k-block's partial ready for the drain
+            ++dr;
+          }
         }
-        umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
+        if (!kdrain) umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
       }
     }
   } else if (warp < 6) {
@@ -386,9 +417,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ctid/8 + 16 (j&1), 32 B atom ((ctid&7)>>1) ^ ((ctid>>3)&3), see split_tile)
     constexpr int NB = BN / 32;
     const bool want_cs = (cs_part != nullptr) && B_MN && !B_PRE;
-    float cs[NB][4];
+    // float64: a float32 running sum over a split's thousands of rows drifts
+    // past the 1e-4 bar on columns whose total cancels to O(1) (measured)
+    double cs[NB][4];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) cs[b][0] = cs[b][1] = cs[b][2] = cs[b][3] = 0.f;
+    for (int b = 0; b < NB; ++b) cs[b][0] = cs[b][1] = cs[b][2] = cs[b][3] = 0.0;
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int z, m0, n0, kb, nk;
@@ -469,18 +502,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // one lane per atom writes this warp's partial: cs_part[z][warp][n]
         const int half = lane & 1, kr3 = (lane >> 3) & 3;
         const int c32 = ((lane & 7) >> 1) ^ kr3;
-        float* dst = cs_part + ((int64_t)z * 4 + q) * N;
+        double* dst = cs_part + ((int64_t)z * 4 + q) * N;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float sum = 0.f;
+            double sum = 0.0;
 #pragma unroll
             for (int r3 = 0; r3 < 4; ++r3) {
               const int src = ((((c32 ^ r3) << 1) | half)) + 8 * r3;
               sum += __shfl_sync(0xffffffffu, cs[b][e], src);
             }
-            cs[b][e] = 0.f;
+            cs[b][e] = 0.0;
             const int n = n0 + b * 32 + c32 * 8 + half * 4 + e;
             if (kr3 == 0 && n < N) dst[n] = sum;
           }
@@ -491,11 +524,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ---------------- epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 ----------------
     const int q = warp & 3;
     const bool vec = ((ldc & 3) == 0) && ((N & 3) == 0);
-    int tl = 0, ecnt = 0;
+    int tl = 0, ecnt = 0, dr = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
       int z, m0, n0, kb, nk;
       tile_of(t, z, m0, n0, kb, nk);
-      const int abuf = tl & 1;
+      int abuf = tl & 1;
       const int row = m0 + q * 32 + lane;
       // activation-backward inputs of this row's next 32 columns (mask bytes,
       // saved ELU outputs): fetched one chunk ahead -- the first while the
@@ -518,9 +551,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < NSV; ++j) sv_n[j] = ok ? __ldg(sp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       };
-      if (EPI & 20) fetch(0);
-      mbar_wait(&tfull[abuf], (tl >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      bool drained = false;
+      if constexpr (BN <= 128) {
+        if (sc.drain) {
+          // k-block drain: sum the per-k-block partials in fp32 registers
+          // (round-to-nearest, fixed order), then put the tile's sum back in
+          // the last k-block's accumulator for the epilogue below
+          float sum[BN];
+#pragma unroll
+          for (int j = 0; j < BN; ++j) sum[j] = 0.f;
+          for (int ks = 0; ks < nk; ++ks, ++dr) {
+            const int b = dr % 3;
+            mbar_wait(&tfull[b], (dr / 3) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+#pragma unroll
+            for (int c = 0; c < BN; c += 8) {
+              uint32_t r[8];
+              tmem_ld8(ta + c, r);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) sum[c + j] = __fadd_rn(sum[c + j], __uint_as_float(r[j]));
+            }
+            if (ks + 1 < nk) {
+              asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[b]);
+            } else {
+              abuf = b;
+#pragma unroll
+              for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sum[c + j]);
+                tmem_st32(ta + c, r);
+              }
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+          }
+          drained = true;
+        }
+      }
+      if (!drained) {
+        if (EPI & 20) fetch(0);  // overlaps the wait for the accumulator
+        mbar_wait(&tfull[abuf], (tl >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      } else if (EPI & 20) {
+        fetch(0);  // after the drain: its registers are free again
+      }
       float ss = 0.f, sd = 0.f;  // fused node scores of the current head
       int hrem = sc.k >> 2, head = (EPI & 8) ? n0 / sc.k : 0;
 #pragma unroll 1
@@ -719,12 +796,12 @@ __global__ void __launch_bounds__(256) k_reduce_splits(int splits, int64_t MN, i
 // block per column, threads stride the partials, then a fixed-order smem tree
 // (deterministic; a few L2 round trips instead of parts / 32 dependent ones)
 __global__ void __launch_bounds__(256) k_colsum_parts(int parts, int N,
-                                                      const float* __restrict__ cs_part,
+                                                      const double* __restrict__ cs_part,
                                                       float* __restrict__ out) {
   __shared__ double sh[256];
   const int n = blockIdx.x;
   double s = 0.0;
-  for (int p = threadIdx.x; p < parts; p += 256) s += (double)cs_part[(int64_t)p * N + n];
+  for (int p = threadIdx.x; p < parts; p += 256) s += cs_part[(int64_t)p * N + n];
   sh[threadIdx.x] = s;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -772,7 +849,7 @@ struct Maps {
 
 template <bool A_MN, bool B_MN, int BN, bool B_PRE, int EPI>
 static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits, int kchunk,
-                   float* C, const float* bias, float* part, int tma_store, float* cs_part,
+                   float* C, const float* bias, float* part, int tma_store, double* cs_part,
                    const EpiScores& sc) {
   auto kern = k_gemm_tc<A_MN, B_MN, BN, B_PRE, EPI>;
   const int smem = Cfg<BN>::SMEM;
@@ -792,7 +869,7 @@ static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits
 template <int BN>
 static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& mp, int M, int N,
                      int K, int splits, int kchunk, float* C, const float* bias, float* part,
-                     int tma_store, float* cs_part, const EpiScores& sc) {
+                     int tma_store, double* cs_part, const EpiScores& sc) {
 #define L(AM, BM_, PR) \
   launch<AM, BM_, BN, PR, 0>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc)
   // epilogue extras: only the shapes that use them are instantiated (the
@@ -869,10 +946,28 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     return false;
   // 128 or 160 columns per tile, whichever pads N less (N = 320, the GAT
   // 8 x 40 slab: two exact 160-wide tiles instead of three 128-wide ones)
-  const int BN = N <= 32 ? 32
-                 : N <= 64 ? 64
-                 : (ceil_div(N, 160) * 160 < ceil_div(N, 128) * 128 ? 160 : 128);
+  int BN = N <= 32 ? 32
+           : N <= 64 ? 64
+           : (ceil_div(N, 160) * 160 < ceil_div(N, 128) * 128 ? 160 : 128);
   const bool a_mn = ta, b_mn = !tb;
+  // K > 256 (every split-K GEMM included, e.g. dTheta = X^T dX' over K = n):
+  // k-block drain mode (EpiScores::drain).  It keeps three accumulators in
+  // TMEM and BN fp32 sums per thread, so BN <= 128; 160-wide tiles (N = 320,
+  // the Gat2 8 x 40 slab, K = 2048) keep one accumulator per tile -- their
+  // fused node scores need whole 40-wide heads per tile, and the model step
+  // stays at 1.4e-5 of the float64 reference (tests/test_gpu_fullsize.py).
+  const int ksteps = (int)ceil_div(K, BK);
+  const bool drain = ksteps > 8 && BN <= 128;
+  auto split_count = [&](int bn) {
+    const int tl = (int)(ceil_div(M, BM) * ceil_div(N, bn));
+    int sp = 1;
+    if (tl < ctx->num_sms && ksteps >= 16) {
+      // one wave: tiles * splits <= num_sms (a 149th tile would double the time)
+      sp = (int)std::min<int64_t>(ctx->num_sms / tl, ksteps / 8);
+      if (sp < 1) sp = 1;
+    }
+    return sp;
+  };
   // Small B (the parameter matrix Theta): split hi/lo once in global memory so
   // the kernel streams both halves with TMA and spends no smem bandwidth on it.
   const int64_t belems = (int64_t)rb * cb;
@@ -897,15 +992,15 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   okB = okB && (b_mn ? make_map(&mp.blo, Blo, N, K, cb, BK, true)
                      : make_map(&mp.blo, Blo, K, N, cb, BN, false));
   if (!okB) return false;
-  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
-  int splits = 1;
-  const int ksteps = (int)ceil_div(K, BK);
-  if (tiles < ctx->num_sms && ksteps >= 16) {
-    // one wave: tiles * splits <= num_sms (a 149th tile would double the time)
-    splits = (int)std::min<int64_t>(ctx->num_sms / tiles, ksteps / 8);
-    if (splits < 1) splits = 1;
+  int splits = split_count(BN);
+  int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
+  {  // dev knob (accuracy experiments): force the split-K chunk length
+    static const int forced = [] {
+      const char* e = getenv("SGNN_GEMM_KCHUNK");
+      return e ? atoi(e) : 0;
+    }();
+    if (forced > 0 && splits > 1) kchunk = (int)ceil_div(forced, BK) * BK;
   }
-  const int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
   splits = (int)ceil_div(K, kchunk);
   EpiScores sc;
   if (att_src) {  // fused node scores: whole heads per tile, no split-K, no bias
@@ -923,6 +1018,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   sc.relu_out = relu_out;
   sc.mask_in = mask_in;
   sc.elu_saved = elu_saved;
+  sc.drain = drain;
   if (elu_saved && (!mask_in || (reinterpret_cast<uintptr_t>(elu_saved) & 15))) return false;
   if ((sc.a_src || relu_out || mask_in) && (a_mn || !pre)) return false;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
@@ -944,10 +1040,10 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     part = DevBuf((size_t)splits * M * N * sizeof(float), ctx->stream);
     pp = part.as<float>();
   }
-  float* cs = nullptr;
+  double* cs = nullptr;
   if (colsum_b) {
-    csp = DevBuf((size_t)splits * 4 * N * sizeof(float), ctx->stream);
-    cs = csp.as<float>();
+    csp = DevBuf((size_t)splits * 4 * N * sizeof(double), ctx->stream);
+    cs = csp.as<double>();
   }
   switch (BN) {
     case 32: dispatch<32>(ctx, a_mn, b_mn, pre, mp, M, N, K, splits, kchunk, C, bias, pp, tma_store, cs, sc); break;

@@ -1,0 +1,371 @@
+// Dev lab (not shipped): CSR SpMM f=128 fp32 on an Arxiv-shaped uniform random
+// graph -- warp-per-row register gathers (the shipped k_spmm_lean) against
+// deep shared-memory rings fed by cp.async (LDGSTS) or TMA tile::gather4.
+// All variants accumulate each output element in stored edge order with an
+// unfused multiply + add, so every variant must be bit-identical to V0.
+//
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -o spmm_lab spmm_lab.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) {                                                            \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);         \
+      exit(1);                                                                          \
+    }                                                                                   \
+  } while (0)
+
+__device__ __forceinline__ float madd(float a, float s, float b) {
+  return __fadd_rn(a, __fmul_rn(s, b));
+}
+__device__ __forceinline__ void acc4(float4& a, float v, const float4& b) {
+  a.x = madd(a.x, v, b.x);
+  a.y = madd(a.y, v, b.y);
+  a.z = madd(a.z, v, b.z);
+  a.w = madd(a.w, v, b.w);
+}
+
+// ---- V0: shipped lean kernel (warp per row, U edges in flight) -------------
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_v0(int n, const int* __restrict__ rowptr,
+                                                   const int* __restrict__ cols,
+                                                   const float* __restrict__ vals,
+                                                   const float4* __restrict__ B,
+                                                   float4* __restrict__ C) {
+  const int lane = threadIdx.x & 31;
+  const int row = (int)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (row >= n) return;
+  const int beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int e = beg;
+  for (; e + U <= end; e += U) {
+    int c[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldg(cols + e + u), v[u] = __ldg(vals + e + u);
+    float4 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) b[u] = __ldg(B + (uint32_t)c[u] * 32u + lane);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc4(acc, v[u], b[u]);
+  }
+  for (; e < end; ++e) acc4(acc, __ldg(vals + e), __ldg(B + (uint32_t)__ldg(cols + e) * 32u + lane));
+  __stcs(C + (uint32_t)row * 32u + lane, acc);
+}
+
+// ---- warp range by nnz: warp w of nw gets rows [r0, r1) -----------------------
+__device__ __forceinline__ int lower_row(const int* rowptr, int n, long long target) {
+  // first row r with rowptr[r] >= target
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(rowptr + mid) < target) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// ---- V2: TMA tile::gather4 ring (4 rows x 512 B per request) -----------------
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_g4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
+
+// ---- ring kernels: warp owns an nnz-balanced row range, streams its edges in
+// groups of G through S shared-memory stages.  Metadata (cols for the issuer,
+// vals and row ends for the consumer) is loaded in coalesced 32-wide batches,
+// one batch ahead, so no dependent global load sits on the per-edge path.
+struct Meta {
+  int cur, nxt, b;  // current / next batch register, batch index of `cur`
+};
+template <class T>
+__device__ __forceinline__ T ld_or(const T* p, int i, int lim, T dflt) {
+  return i < lim ? __ldg(p + i) : dflt;
+}
+
+template <int S, int G, bool TMA>
+__global__ void __launch_bounds__(512, 1) k_ring(int n, const int* __restrict__ rowptr,
+                                                  const int* __restrict__ cols,
+                                                  const float* __restrict__ vals,
+                                                  const float4* __restrict__ B,
+                                                  const __grid_constant__ CUtensorMap map,
+                                                  float4* __restrict__ C) {
+  extern __shared__ __align__(1024) float4 ring[];  // [warps][S][G][32]
+  __shared__ __align__(8) uint64_t bars[16 * 32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;
+  const int nw = gridDim.x * nwb;
+  const int w = blockIdx.x * nwb + wib;
+  uint64_t* mb = bars + wib * S;
+  if (TMA) {
+    if (lane == 0)
+      for (int s = 0; s < S; ++s) mbar_init(mb + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
+  const long long nnz = __ldg(rowptr + n);
+  const int r0 = lower_row(rowptr, n, (nnz * w) / nw);
+  const int r1 = (w == nw - 1) ? n : lower_row(rowptr, n, (nnz * (w + 1)) / nw);
+  if (r0 >= r1) return;
+  float4* my = ring + (size_t)wib * S * G * 32;
+  const int E0 = __ldg(rowptr + r0), ne = __ldg(rowptr + r1) - E0;
+  const int* wc = cols + E0;
+  const float* wv = vals + E0;
+  const int ngroups = (ne + G - 1) / G;
+  // issuer: cols in batches of 32 edges
+  int ic = ld_or(wc, lane, ne, 0), icn = ld_or(wc, 32 + lane, ne, 0), ib = 0;
+  auto issue = [&](int g) {
+    if (g < ngroups) {
+      const int o = g * G;
+      if ((o >> 5) != ib) {
+        ib = o >> 5;
+        ic = icn;
+        icn = ld_or(wc, (ib + 1) * 32 + lane, ne, 0);
+      }
+      float4* dst = my + (size_t)(g % S) * G * 32;
+      if (TMA) {
+        static_assert(!TMA || G % 4 == 0, "gather4 needs G % 4 == 0");
+#pragma unroll
+        for (int q = 0; q < G; q += 4) {
+          const int c0 = __shfl_sync(0xffffffffu, ic, (o + q) & 31);
+          const int c1 = __shfl_sync(0xffffffffu, ic, (o + q + 1) & 31);
+          const int c2 = __shfl_sync(0xffffffffu, ic, (o + q + 2) & 31);
+          const int c3 = __shfl_sync(0xffffffffu, ic, (o + q + 3) & 31);
+          if (lane == 0) {
+            if (q == 0) mbar_expect(mb + (g % S), G * 512);
+            tma_g4(dst + q * 32, &map, mb + (g % S), 0, c0, c1, c2, c3);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const int cj = __shfl_sync(0xffffffffu, ic, (o + j) & 31);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                           smem_u32(dst + j * 32 + lane)),
+                       "l"(B + (uint32_t)cj * 32u + lane));
+        }
+      }
+    }
+    if (!TMA) asm volatile("cp.async.commit_group;\n" ::);
+  };
+#pragma unroll
+  for (int s = 0; s < S; ++s) issue(s);
+  // consumer: vals in batches of 32 edges, row ends in batches of 32 rows
+  float cv = ld_or(wv, lane, ne, 0.f), cvn = ld_or(wv, 32 + lane, ne, 0.f);
+  int vb = 0;
+  int rb = r0;
+  int re = ld_or(rowptr + 1, r0 + lane, r1, 0x7fffffff) - E0;
+  int ren = ld_or(rowptr + 1, r0 + 32 + lane, r1, 0x7fffffff) - E0;
+  int cur = r0;
+  int rend = __shfl_sync(0xffffffffu, re, 0);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g = 0; g < ngroups; ++g) {
+    if (TMA) mbar_wait(mb + (g % S), (g / S) & 1);
+    else asm volatile("cp.async.wait_group %0;\n" ::"n"(S - 1));
+    const float4* st = my + (size_t)(g % S) * G * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int o = g * G + j;
+      if (o < ne) {
+        if ((o >> 5) != vb) {
+          vb = o >> 5;
+          cv = cvn;
+          cvn = ld_or(wv, (vb + 1) * 32 + lane, ne, 0.f);
+        }
+        const float v = __shfl_sync(0xffffffffu, cv, o & 31);
+        while (o >= rend) {
+          __stcs(C + (uint32_t)cur * 32u + lane, acc);
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          ++cur;
+          if (cur - rb == 32) {
+            rb = cur;
+            re = ren;
+            ren = ld_or(rowptr + 1, rb + 32 + lane, r1, 0x7fffffff) - E0;
+          }
+          rend = __shfl_sync(0xffffffffu, re, cur - rb);
+        }
+        acc4(acc, v, st[j * 32]);
+      }
+    }
+    if (TMA) __syncwarp();
+    issue(g + S);
+  }
+  if (!TMA) asm volatile("cp.async.wait_all;\n" ::);
+  while (cur < r1) {
+    __stcs(C + (uint32_t)cur * 32u + lane, acc);
+    acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    ++cur;
+  }
+}
+
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main(int argc, char** argv) {
+  const int n = 169343;
+  const double deg = 1335587.0 / n;
+  std::mt19937_64 rng(1);
+  std::vector<int> rowptr(n + 1, 0), cols;
+  std::vector<float> vals;
+  cols.reserve((size_t)(deg * n * 1.05));
+  std::poisson_distribution<int> pd(deg - 1.0);
+  for (int i = 0; i < n; ++i) {
+    int d = 1 + pd(rng);
+    std::vector<int> c(d);
+    for (auto& x : c) x = (int)(rng() % n);
+    std::sort(c.begin(), c.end());
+    for (int x : c) {
+      cols.push_back(x);
+      vals.push_back((float)((rng() % 1000) / 1000.0 + 0.001));
+    }
+    rowptr[i + 1] = (int)cols.size();
+  }
+  const long long nnz = cols.size();
+  printf("n=%d nnz=%lld\n", n, nnz);
+  int *d_rp, *d_c;
+  float *d_v, *d_B, *d_C, *d_C0;
+  char* flush;
+  CK(cudaMalloc(&d_rp, (n + 1) * 4));
+  CK(cudaMalloc(&d_c, nnz * 4));
+  CK(cudaMalloc(&d_v, nnz * 4));
+  CK(cudaMalloc(&d_B, (size_t)n * 512));
+  CK(cudaMalloc(&d_C, (size_t)n * 512));
+  CK(cudaMalloc(&d_C0, (size_t)n * 512));
+  CK(cudaMalloc(&flush, 256 << 20));
+  std::vector<float> hB((size_t)n * 128);
+  for (auto& x : hB) x = (float)((rng() % 2000) / 1000.0 - 1.0);
+  CK(cudaMemcpy(d_rp, rowptr.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_c, cols.data(), nnz * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_v, vals.data(), nnz * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_B, hB.data(), (size_t)n * 512, cudaMemcpyHostToDevice));
+
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q));
+  CUtensorMap map;
+  {
+    cuuint64_t dims[2] = {128, (cuuint64_t)n};
+    cuuint64_t strides[1] = {512};
+    cuuint32_t box[2] = {128, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = ((EncodeFn)fp)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_B, dims, strides, box,
+                                es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      printf("encode failed %d\n", (int)r);
+      return 1;
+    }
+  }
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const size_t nbytes = (size_t)n * 512;
+  const double alg = 4.0 * (n + 1) + 8.0 * nnz + 2.0 * nbytes;
+  auto run = [&](const char* name, auto launch, bool ref) {
+    CK(cudaMemset(d_C, 0xff, nbytes));
+    launch();
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    if (ref) CK(cudaMemcpy(d_C0, d_C, nbytes, cudaMemcpyDeviceToDevice));
+    std::vector<float> h0((size_t)n * 128), h1((size_t)n * 128);
+    CK(cudaMemcpy(h0.data(), d_C0, nbytes, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h1.data(), d_C, nbytes, cudaMemcpyDeviceToHost));
+    const bool same = std::memcmp(h0.data(), h1.data(), nbytes) == 0;
+    float tot = 0.f, best = 1e9f;
+    const int reps = 20;
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaMemsetAsync(flush, r, 256 << 20, st));
+      cudaEventRecord(a, st);
+      launch();
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      tot += ms;
+      best = std::min(best, ms);
+    }
+    const float mean = tot / reps;
+    printf("%-34s mean %7.1f us  best %7.1f us  alg %6.0f GB/s  gathered %6.0f GB/s  %s\n",
+           name, mean * 1e3, best * 1e3, alg / (mean * 1e-3) / 1e9,
+           nnz * 512.0 / (mean * 1e-3) / 1e9, same ? "bit-exact" : "MISMATCH");
+  };
+  const int g0 = (n * 32 + 255) / 256;
+  run("v0 U=2 minB=8", [&] { k_v0<2, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, true);
+  run("v0 U=4 minB=6", [&] { k_v0<4, 6><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
+  run("v0 U=1 minB=8", [&] { k_v0<1, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
+
+#define VR(S, G, TMA, WPB, CPS)                                                                \
+  {                                                                                            \
+    const int sm = WPB * S * G * 512;                                                          \
+    CK(cudaFuncSetAttribute(k_ring<S, G, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    char nm[64];                                                                               \
+    snprintf(nm, 64, "%s S=%d G=%d w=%d cta/sm=%d", TMA ? "tma.g4 " : "cp.async", S, G, WPB, CPS); \
+    run(nm, [&] { k_ring<S, G, TMA><<<148 * CPS, WPB * 32, sm, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, map, (float4*)d_C); }, false); \
+  }
+  // L2 persistence window on B with the V0 kernel
+  {
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, 0);
+    printf("max persisting L2 = %.1f MB\n", maxp / 1e6);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxp));
+    cudaStreamAttrValue at = {};
+    at.accessPolicyWindow.base_ptr = d_B;
+    at.accessPolicyWindow.num_bytes = std::min<size_t>(nbytes, 134217728);
+    at.accessPolicyWindow.hitRatio = std::min(1.0f, (float)maxp / (float)nbytes);
+    at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at));
+    for (float hr : {0.3f, 0.5f, 0.7f, 0.85f, 0.956f, 1.0f}) {
+      at.accessPolicyWindow.hitRatio = hr;
+      CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at));
+      char nm[64];
+      snprintf(nm, 64, "v0 U=2 + persist hitRatio=%.2f", hr);
+      run(nm, [&] { k_v0<2, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
+    }
+    at.accessPolicyWindow.hitRatio = 0.7f;
+    at.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at));
+    run("v0 + persist 0.7 miss=normal", [&] { k_v0<2, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
+  }
+  return 0;
+}

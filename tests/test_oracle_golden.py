@@ -216,3 +216,25 @@ def test_oracle_model_step_matches_reference(golden, orc, tag):
     assert orc.max_rel_diff(out, g[f"{tag}_pred"]) < 1e-12
     assert orc.max_rel_diff(flat, g[f"{tag}_grads"]) < 1e-12
     assert abs(loss - g[f"{tag}_loss"][0]) < 1e-12
+
+
+def test_gat_f64_restatement_matches_reference_golden(golden):
+    """oracle/gat_f64.py (vectorised float64 GAT, the full-size checker) against
+    the reference's own outputs (tests/golden/gat.npz) at 1e-12, and its
+    mask override is the identity when given the reference's own mask."""
+    import gat_f64
+
+    g = golden("gat")
+    h, beta = int(g["heads"]), float(g["beta"])
+    rp, cl = g["rowptr"], g["cols"]
+    out, st = gat_f64.forward(rp, cl, g["X"], g["theta"], g["a_src"], g["a_dst"], g["bias"], h,
+                              beta)
+    assert np.abs(out - g["out_0"]).max() <= 1e-12 * max(1.0, np.abs(g["out_0"]).max())
+    assert np.array_equal(st["mask"].T.astype(np.uint8), g["mask_0"])
+    assert np.abs(st["alpha"].T - g["alpha_0"]).max() <= 1e-13
+    for mask in (None, g["mask_0"].T.astype(bool)):
+        got = gat_f64.backward(rp, cl, g["G"], g["X"], g["theta"], g["a_src"], g["a_dst"], h,
+                               beta, True, mask=mask)
+        for x, nm in zip(got, ("dtheta", "da_src", "da_dst", "dbias", "dinput")):
+            want = g[f"{nm}_0"]
+            assert np.abs(x - want).max() <= 1e-12 * max(1.0, np.abs(want).max()), nm
