@@ -59,22 +59,30 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-# component of the step -> kernel name in the committed ncu capture
-_KERNEL_OF = {"spmm_fwd_f128": "k_spmm_lean<1, 2>", "spmm_bwd_f128": "k_spmm_lean<1, 2>",
-              "gemm_PxTheta": "tc::k_gemm_tc<0, 0, 128, 1>",
-              "gemm_GThetaT": "tc::k_gemm_tc<0, 1, 128, 1>",
-              "colsum_db": "k_colsum_partial<float>"}
+# component of the step -> kernel (name prefix) in the committed ncu capture
+_KERNEL_OF = {"spmm_fwd_f128": "k_spmm_lean<1, 2", "spmm_bwd_f128": "k_spmm_lean<1, 2",
+              "gemm_PxTheta": "tc::k_gemm_tc<0, 1, 128, 1", "gemm_PtG": "tc::k_gemm_tc<1, 1, 128, 0",
+              "gemm_GThetaT": "tc::k_gemm_tc<0, 0, 128, 1",
+              "colsum_db": "k_colsum_partial", "gat_col2": "g2::k_gat_col2<8, 2",
+              "gat_sddmm2": "g2::k_gat_sddmm2<8, 2", "gat_agg2": "g2::k_gat_agg2<8, 2"}
 
 
 def _traffic(component):
-    """DRAM bytes per launch of the component's kernel from the committed
-    `ncu --set full` capture (profiles/traffic.json, scripts/summarize_profiles.py)."""
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    component's kernel in the committed `ncu --set full` capture
+    (profiles/traffic.json, written by scripts/summarize_profiles.py); None if
+    the capture does not hold it."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             t = json.load(fh)
-        return int(t["kernels"][_KERNEL_OF[component]] * 1e6)
+        pre = _KERNEL_OF[component]
+        for name, mb in t["kernels"].items():
+            if name.startswith(pre) or name.split("::")[-1].startswith(pre.split("::")[-1]):
+                return {"bytes": int(mb * 1e6), "source": f"profiles/traffic.json ({t['tag']}): "
+                                                          f"{name}"}
     except Exception:
-        return None
+        pass
+    return None
 
 
 class Clocks:
@@ -195,6 +203,60 @@ def _config():
 
 
 # ---------------------------------------------------------------------------
+# parity of the timed steps (outside the timed region): the GCN step's four
+# outputs against the reference itself in float64 (oracle/_ref, the
+# unmodified headers compiled in place), and the GAT layer against the
+# float64 restatement pinned to it (oracle/gat_f64.py) evaluated with the
+# device's LeakyReLU decisions (the ill-conditioned sign flips at y ~ 0 are
+# counted and must all sit at |y| < 1e-5 of the score scale)
+# ---------------------------------------------------------------------------
+def step_parity(d, A, P, X, G, theta, bias, scheme, th_g, as_g, ad_g, b_g, Gg, src, dst):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import gat_f64
+        import oracle as orc
+        import refpy
+    except Exception as ex:  # noqa: BLE001
+        return {"unavailable": str(ex)}
+    h64 = lambda t: t.detach().double().cpu().numpy()  # noqa: E731
+    n = ARXIV_N
+    res = {"bar": 1e-4, "metric": "max_rel_diff (dense.hpp:303-316)"}
+    try:
+        out, cache = d.gcn_forward(A, X, theta, bias, scheme)
+        got = (out,) + d.gcn_backward(A, G, theta, cache, True)
+        coo = refpy.gcn_normalize(n, src.numpy(), dst.numpy())
+        want = refpy.gcn_layer(n, coo, 2, h64(X), h64(theta), h64(bias),
+                               (scheme.forward, scheme.backward, scheme.caching), h64(G), True)
+        res["gcn_step"] = {nm: float(f"{orc.max_rel_diff(h64(g), w):.3e}")
+                           for nm, g, w in zip(("out", "d_theta", "d_bias", "d_input"), got, want)}
+        res["gcn_reference"] = "oracle/_ref float64 (reference headers, CSC)"
+    except Exception as ex:  # noqa: BLE001
+        res["gcn_step"] = f"unavailable: {ex}"
+    try:
+        o, c = d.gat_forward(P, X, th_g, as_g, ad_g, b_g, GAT_H, 0.2, "full")
+        _, mk = c.edge_values(P, th_g, as_g, ad_g)
+        got = (o,) + d.gat_backward(P, Gg, th_g, as_g, ad_g, c, True)
+        pa = P.arrays()
+        rp, cl = pa["rowptr"].cpu().numpy(), pa["cols"].cpu().numpy()
+        args = [h64(x) for x in (X, th_g, as_g, ad_g, b_g)]
+        dm = mk.t().cpu().numpy().astype(bool)
+        wo, st = gat_f64.forward(rp, cl, *args, GAT_H)
+        flips, far = gat_f64.ill_conditioned_flips(st["y"], dm)
+        wg = gat_f64.backward(rp, cl, h64(Gg), *args[:4], GAT_H, fg=True, mask=dm)
+        names = ("out", "d_theta", "d_a_src", "d_a_dst", "d_bias", "d_input")
+        res["gat_layer"] = {nm: float(f"{orc.max_rel_diff(h64(g), w):.3e}")
+                            for nm, g, w in zip(names, got, (wo,) + wg)}
+        res["gat_leaky_relu_flips"] = {"count": flips, "at_or_above_1e-5_scale": far}
+    except Exception as ex:  # noqa: BLE001
+        res["gat_layer"] = f"unavailable: {ex}"
+    vals = [v for k in ("gcn_step", "gat_layer") if isinstance(res.get(k), dict)
+            for v in res[k].values()]
+    res["max"] = max(vals) if vals else None
+    res["pass"] = bool(vals) and max(vals) <= 1e-4
+    return res
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args):
@@ -295,9 +357,12 @@ def run_ours(args):
         gemm_bytes.get(dominant, 4 * n * K_OUT))
     achieved = dom_bytes / (comps[dominant] * 1e-3) / 1e9
     spmm_gbs = spmm_bytes / (comps["spmm_fwd_f128"] * 1e-3) / 1e9
+    tr = _traffic(dominant)
     roofline = {"kernel": dominant, "bound": "hbm", "achieved": round(achieved, 1),
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": _traffic(dominant), "algorithmic_bytes": dom_bytes, "peak_source": peak_kind,
+                "traffic": tr["bytes"] if tr else None, "algorithmic_bytes": dom_bytes,
+                "traffic_over_algorithmic": round(tr["bytes"] / dom_bytes, 3) if tr else None,
+                "traffic_source": tr["source"] if tr else None, "peak_source": peak_kind,
                 "ms": round(comps[dominant], 4)}
     if dominant.startswith("spmm"):
         # the SpMM gathers one dense row per edge: q' * 512 B of L2->SM traffic;
@@ -338,12 +403,43 @@ def run_ours(args):
     hk = GAT_H * GAT_K
     sd_bytes = 4 * (n + 1) + 4 * P.nnz + 8 * n * hk + 4 * P.nnz * GAT_H
     sd_gbs = sd_bytes / (sd_ms * 1e-3) / 1e9
+    tr = _traffic("gat_sddmm2")
     sddmm_line = {"kernel": "g2::k_gat_sddmm2 (h=8, k=32, Arxiv pattern)", "ms": round(sd_ms, 4),
                   "algorithmic_bytes": sd_bytes, "achieved": round(sd_gbs, 1), "peak": hbm,
                   "unit": "GB/s", "frac": round(sd_gbs / hbm, 4),
+                  "traffic": tr["bytes"] if tr else None,
+                  "traffic_over_algorithmic": round(tr["bytes"] / sd_bytes, 3) if tr else None,
                   "gathered_bytes": P.nnz * hk * 4,
                   "gather_frac_of_173MB_probe": round(P.nnz * hk * 4 / (sd_ms * 1e-3) / 1e9
                                                       / 8561.0, 4)}
+
+    # ---- the GAT step's dominant kernel alone: the column pass ---------------
+    # (kernels.hpp:258-295 + 614-658: dM = alpha^T dX' + dS a_src + dD a_dst and
+    # dD = column sums of dy, over the CSC view).  Algorithmic bytes (DESIGN 3):
+    # 4(n+1) + 8q' (colptr, rows, perm) + 8q'h (alpha, dy) + 8n.hk (dX' once,
+    # dM once) + 8nh (dS in, dD out)
+    import ctypes as _C
+    al = torch.rand((P.nnz, GAT_H), dtype=torch.float32, device=dev) * 0.2
+    dyv = torch.randn((P.nnz, GAT_H), dtype=torch.float32, device=dev) * 0.1
+    dSv = torch.randn((n, GAT_H), dtype=torch.float32, device=dev)
+    dDv = torch.empty((n, GAT_H), dtype=torch.float32, device=dev)
+    dMv = torch.empty((n, hk), dtype=torch.float32, device=dev)
+    vp = lambda t: _C.c_void_p(t.data_ptr())  # noqa: E731
+
+    def colpass():
+        capi.check(capi.lib.sgnn_gat_column_pass(
+            ctx.handle, n, vp(pa["colptr"]), vp(pa["rows"]), vp(pa["perm"]), GAT_H, GAT_K,
+            vp(Gg), vp(al), vp(dyv), vp(dSv), vp(as_g), vp(ad_g), vp(dDv), vp(dMv), None))
+
+    cp_ms = statistics.mean(timed(colpass, reps, 2))
+    cp_bytes = 4 * (n + 1) + 8 * P.nnz + 8 * P.nnz * GAT_H + 8 * n * hk + 8 * n * GAT_H
+    cp_gbs = cp_bytes / (cp_ms * 1e-3) / 1e9
+    tr = _traffic("gat_col2")
+    gat_roofline = {"kernel": "g2::k_gat_col2 (h=8, k=32, Arxiv pattern)", "bound": "hbm",
+                    "ms": round(cp_ms, 4), "algorithmic_bytes": cp_bytes,
+                    "achieved": round(cp_gbs, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(cp_gbs / hbm, 4), "traffic": tr["bytes"] if tr else None,
+                    "traffic_over_algorithmic": round(tr["bytes"] / cp_bytes, 3) if tr else None}
 
     # ---- 2-layer models, full training step with MSE (config 4) -------------
     gcn2 = d.Model("gcn2", M_IN, GCN2_HID, MODEL_OUT, scheme="adaptive", caching=True,
@@ -395,6 +491,8 @@ def run_ours(args):
             dist.barrier()
             dist.destroy_process_group()
         return
+    parity = None if args.no_parity else step_parity(d, A, P, X, G, theta, bias, scheme, th_g,
+                                                     as_g, ad_g, b_g, Gg, src, dst)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -420,9 +518,11 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generators, device-side)",
-        "config": dict(_config(), scheme=str(scheme), nnz=q,
-                       execution="CUDA graph replay of the captured step (eager launches: "
-                                 f"{round(eager_ms, 4)} ms)"),
+        "config": _config(),
+        "scheme": str(scheme), "nnz": q,
+        "execution": f"CUDA graph replay of the captured step (eager launches: "
+                     f"{round(eager_ms, 4)} ms)",
+        "parity": parity,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
@@ -435,6 +535,7 @@ def run_ours(args):
         "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K, "level": "full",
                       "nnz": P.nnz},
         "sddmm": sddmm_line,
+        "gat_roofline": gat_roofline,
         "models": models,
         "setup_s": round(setup_s, 2),
     }
@@ -593,8 +694,9 @@ def run_ours_dist(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(mean_ms, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (reference generators, device-side)",
-            "config": dict(_config(), scheme=str(s), nnz=int(r.numel()),
-                           parallelism=f"row-partition x{world} (NCCL all-gather/all-reduce)"),
+            "config": _config(),
+            "scheme": str(s), "nnz": int(r.numel()),
+            "parallelism": f"row-partition x{world} (NCCL all-gather/all-reduce)",
             "clocks": clk.summary(),
             "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -623,6 +725,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-model-cpu", action="store_true",
                     help="skip the reference's CPU timing of the 2-layer model steps")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-timing parity check against the reference")
     ap.add_argument("--dist", action="store_true",
                     help="use the row-partitioned multi-GPU path even at WORLD_SIZE=1")
     args = ap.parse_args()
