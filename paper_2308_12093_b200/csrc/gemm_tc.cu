@@ -134,11 +134,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                 "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
@@ -417,11 +420,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ctid/8 + 16 (j&1), 32 B atom ((ctid&7)>>1) ^ ((ctid>>3)&3), see split_tile)
     constexpr int NB = BN / 32;
     const bool want_cs = (cs_part != nullptr) && B_MN && !B_PRE;
-    // float64: a float32 running sum over a split's thousands of rows drifts
-    // past the 1e-4 bar on columns whose total cancels to O(1) (measured)
+    // float32 within 8 k-blocks (16 rows per thread), then float64: one
+    // float32 running sum over a split's thousands of rows drifts past the
+    // 1e-4 bar on columns whose total cancels to O(1) (measured), and a
+    // float64 add per element costs the converters 20 us on dTheta
     double cs[NB][4];
+    float cf[NB][4];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) cs[b][0] = cs[b][1] = cs[b][2] = cs[b][3] = 0.0;
+    for (int b = 0; b < NB; ++b) {
+      cs[b][0] = cs[b][1] = cs[b][2] = cs[b][3] = 0.0;
+      cf[b][0] = cf[b][1] = cf[b][2] = cf[b][3] = 0.f;
+    }
+    auto fold_cs = [&] {
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          cs[b][e] += (double)cf[b][e];
+          cf[b][e] = 0.f;
+        }
+    };
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int z, m0, n0, kb, nk;
@@ -438,10 +456,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < CF::B_BYTES / 16 / 128; ++j) {
               const int i = ctid + 128 * j;
               float4 v = raw[i];
-              cs[j >> 1][0] += v.x;
-              cs[j >> 1][1] += v.y;
-              cs[j >> 1][2] += v.z;
-              cs[j >> 1][3] += v.w;
+              cf[j >> 1][0] += v.x;
+              cf[j >> 1][1] += v.y;
+              cf[j >> 1][2] += v.z;
+              cf[j >> 1][3] += v.w;
               float4 h, l;
               h.x = __uint_as_float(tf32_hi(v.x));
               h.y = __uint_as_float(tf32_hi(v.y));
@@ -454,6 +472,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               raw[i] = h;
               lo[i] = l;
             }
+            if ((ks & 7) == 7 || ks + 1 == nk) fold_cs();
           } else {
             split_tile(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
                        CF::B_BYTES / 16, ctid, 128);
@@ -566,11 +585,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll
-            for (int c = 0; c < BN; c += 8) {
-              uint32_t r[8];
-              tmem_ld8(ta + c, r);
+            for (int c = 0; c < BN; c += 16) {
+              uint32_t r[16];
+              tmem_ld16(ta + c, r);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) sum[c + j] = __fadd_rn(sum[c + j], __uint_as_float(r[j]));
+              for (int j = 0; j < 16; ++j)
+                sum[c + j] = __fadd_rn(sum[c + j], __uint_as_float(r[j]));
             }
             if (ks + 1 < nk) {
               asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
