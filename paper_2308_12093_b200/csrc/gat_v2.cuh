@@ -333,93 +333,6 @@ __device__ __forceinline__ uint32_t restage_alpha(int32_t ee, const int32_t* __r
 }
 
 // ---------------------------------------------------------------------------
-// forward, part 1 (kernels.hpp:427-534): attention of every (edge, head),
-// written edge-major (q x h) with the LeakyReLU mask.  A warp owns 32 rows;
-// each thread walks its own row (<= TMAX edges) serially: one online pass for
-// (max, sum) -- the running sum is rescaled when the max grows -- and one pass
-// writing alpha = exp(w - max) * (1 / sum).  The neighbour's score row (h
-// floats) is one 32-byte gather per edge; the second pass hits L1.  Rows
-// longer than TMAX are then done by the whole warp, lanes over edges.
-// ---------------------------------------------------------------------------
-constexpr int TMAX = 32;
-
-template <int H>
-__global__ void __launch_bounds__(256) k_gat_attn3(int32_t n, const int32_t* __restrict__ rowptr,
-                                                   const int32_t* __restrict__ cols,
-                                                   const float* __restrict__ s,
-                                                   const float* __restrict__ d, float beta,
-                                                   float* __restrict__ alpha,
-                                                   uint8_t* __restrict__ mask) {
-  __shared__ float sh_a[WPB][32][H + 1];
-  __shared__ float sh_st[WPB][3][H];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t i = ((int32_t)blockIdx.x * WPB + wib) * 32 + lane;
-  int32_t beg = 0, end = 0;
-  if (i < n) {
-    beg = __ldg(rowptr + i);
-    end = __ldg(rowptr + i + 1);
-  }
-  const bool longrow = end - beg > TMAX;
-  if (i < n && !longrow) {
-    float si[H], mx[H], sm[H];
-    ld_heads<H>(s + (int64_t)i * H, si);
-#pragma unroll
-    for (int t = 0; t < H; ++t) {
-      mx[t] = -INFINITY;
-      sm[t] = 0.f;
-    }
-    for (int32_t e = beg; e < end; ++e) {
-      float dj[H];
-      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
-#pragma unroll
-      for (int t = 0; t < H; ++t) {
-        const float w = lrelu(si[t] + dj[t], beta);
-        const float mn = fmaxf(mx[t], w);
-        sm[t] = sm[t] * expf(mx[t] - mn) + expf(w - mn);
-        mx[t] = mn;
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
-    for (int32_t e = beg; e < end; ++e) {
-      float dj[H], a[H];
-      ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
-      uint32_t pos = 0;
-#pragma unroll
-      for (int t = 0; t < H; ++t) {
-        const float y = si[t] + dj[t];
-        if (y > 0.f) pos |= 1u << t;
-        a[t] = expf(lrelu(y, beta) - mx[t]) * sm[t];
-      }
-      st_heads<H>(alpha + (int64_t)e * H, a);
-      if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
-    }
-  }
-  uint32_t lm = __ballot_sync(0xffffffffu, i < n && longrow);
-  float(*sa)[H + 1] = sh_a[wib];
-  float(*st)[H] = sh_st[wib];
-  while (lm) {
-    const int src = __ffs(lm) - 1;
-    lm &= lm - 1;
-    const int32_t row = __shfl_sync(0xffffffffu, i, src);
-    const int32_t rb = __shfl_sync(0xffffffffu, beg, src);
-    const int32_t re = __shfl_sync(0xffffffffu, end, src);
-    stage_stats<H>(lane, row, rb, re, cols, s, d, beta, sa, st);  // > 32 edges: stats in st
-    for (int32_t ee = rb + lane; ee < re; ee += 32) {
-      float a[H];
-      const uint32_t pos = restage_alpha<H>(ee, cols, d, beta, st, a);
-      st_heads<H>(alpha + (int64_t)ee * H, a);
-      if (mask) st_mask<H>(mask + (int64_t)ee * H, pos);
-    }
-    __syncwarp();
-  }
-}
-
-static inline unsigned attn3_grid(int32_t n) {
-  return (unsigned)((n + 32 * WPB - 1) / (32 * WPB));
-}
-
-// ---------------------------------------------------------------------------
 // forward, part 2 (kernels.hpp:219-254 semibatched SpMM + bias):
 // out[i, t, :] = sum_e alpha[e, t] M[col_e, t, :] + b.  Lean like the GCN
 // SpMM: one warp per row, per edge a broadcast column index, one 4-byte
@@ -759,78 +672,6 @@ __global__ void __launch_bounds__(256, 3)
     }
     for (; off > 0; off >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], off);
     if (writer && e + ou < end) da[(int64_t)(e + ou) * H + ot] = p[0];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// backward, part 2 (kernels.hpp:537-567 softmax backward, 481-495 LeakyReLU
-// backward, 571-588 row sums): per row, dot[t] = sum_e alpha dAlpha, dy =
-// mask ? dw : beta dw with dw = alpha (dAlpha - dot), dS[i, t] = sum_e dy.
-// Thread per row (<= TMAX edges), the whole warp for longer rows.
-// ---------------------------------------------------------------------------
-template <int H>
-__global__ void __launch_bounds__(256) k_gat_sbwd3(int32_t n, const int32_t* __restrict__ rowptr,
-                                                   const float* __restrict__ alpha,
-                                                   const uint8_t* __restrict__ mask,
-                                                   const float* __restrict__ da, float beta,
-                                                   float* __restrict__ dy,
-                                                   float* __restrict__ dS) {
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t i = ((int32_t)blockIdx.x * WPB + wib) * 32 + lane;
-  int32_t beg = 0, end = 0;
-  if (i < n) {
-    beg = __ldg(rowptr + i);
-    end = __ldg(rowptr + i + 1);
-  }
-  const bool longrow = end - beg > TMAX;
-  auto finish = [&](int32_t e, const float (&dot)[H], float (&rs)[H]) {
-    float a[H], g[H], y[H];
-    ld_heads<H>(alpha + (int64_t)e * H, a);
-    ld_heads<H>(da + (int64_t)e * H, g);
-    const uint32_t pos = ld_mask<H>(mask + (int64_t)e * H);
-#pragma unroll
-    for (int t = 0; t < H; ++t) {
-      const float dw = a[t] * (g[t] - dot[t]);
-      y[t] = (pos >> t) & 1u ? dw : beta * dw;
-      rs[t] += y[t];
-    }
-    st_heads<H>(dy + (int64_t)e * H, y);
-  };
-  if (i < n && !longrow) {
-    float dot[H], rs[H];
-#pragma unroll
-    for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
-    for (int32_t e = beg; e < end; ++e) {
-      float a[H], g[H];
-      ld_heads<H>(alpha + (int64_t)e * H, a);
-      ld_heads<H>(da + (int64_t)e * H, g);
-#pragma unroll
-      for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
-    }
-    for (int32_t e = beg; e < end; ++e) finish(e, dot, rs);
-    st_heads<H>(dS + (int64_t)i * H, rs);
-  }
-  uint32_t lm = __ballot_sync(0xffffffffu, i < n && longrow);
-  while (lm) {
-    const int src = __ffs(lm) - 1;
-    lm &= lm - 1;
-    const int32_t row = __shfl_sync(0xffffffffu, i, src);
-    const int32_t rb = __shfl_sync(0xffffffffu, beg, src);
-    const int32_t re = __shfl_sync(0xffffffffu, end, src);
-    float dot[H], rs[H];
-#pragma unroll
-    for (int t = 0; t < H; ++t) dot[t] = rs[t] = 0.f;
-    for (int32_t e = rb + lane; e < re; e += 32) {
-      float a[H], g[H];
-      ld_heads<H>(alpha + (int64_t)e * H, a);
-      ld_heads<H>(da + (int64_t)e * H, g);
-#pragma unroll
-      for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
-    }
-    allreduce<H>(dot, lane, OpSum());
-    for (int32_t e = rb + lane; e < re; e += 32) finish(e, dot, rs);
-    allreduce<H>(rs, lane, OpSum());
-    if (lane == 0) st_heads<H>(dS + (int64_t)row * H, rs);
   }
 }
 
