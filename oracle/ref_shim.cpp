@@ -60,6 +60,26 @@ long long ref_synthetic_graph(int n, double deg, unsigned long long seed, int* s
   return static_cast<long long>(g.edges.size());
 }
 
+// graph.hpp load_graph: returns the edge count (arrays filled when non-null,
+// n in *n), or -1 with the runtime_error text in ref_last_error().
+long long ref_load_graph(const char* path, int matrix_market, int* n, int* src, int* dst,
+                         double* w) {
+  try {
+    Graph g = load_graph(path, matrix_market ? GraphFileFormat::matrix_market
+                                             : GraphFileFormat::edge_list);
+    *n = g.n;
+    for (std::size_t i = 0; i < g.edges.size(); ++i) {
+      if (src) src[i] = g.edges[i].src;
+      if (dst) dst[i] = g.edges[i].dst;
+      if (w) w[i] = g.edges[i].weight;
+    }
+    return static_cast<long long>(g.edges.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void ref_random_uniform(int rows, int cols, unsigned long long seed, double lo, double hi,
                         double* o) {
   out(DenseMatrix<double>::random_uniform(rows, cols, seed, lo, hi), o);

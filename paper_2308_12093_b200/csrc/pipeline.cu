@@ -139,6 +139,8 @@ int sgnn_gat_step_host(sgnn_ctx ctx, sgnn_pattern P, const void* hX, int32_t m,
   SGNN_API_BEGIN
   require(ctx && P && hX && hG, "gat_step_host: null argument");
   require(m >= 1 && heads >= 1 && k >= 1, "gat_forward: input width does not match theta");
+  require(!needs_feature_grad || h_d_input != nullptr,
+          "gat_backward: d_input required for feature gradients");
   const size_t sb = dtype_size(dtype);
   const size_t n = (size_t)P->n, hk = (size_t)heads * k;
   const bool fg = needs_feature_grad != 0;

@@ -97,7 +97,8 @@ int sgnn_powerlaw_graph(sgnn_ctx ctx, int32_t n, double avg_degree, double expon
   *count = 0;
   const int64_t pairs = sgnn_powerlaw_graph_capacity(n, avg_degree) / 2;
   if (pairs == 0) return SGNN_OK;
-  require(pairs < ((int64_t)1 << 31), "powerlaw_graph: too many edges");
+  // 2 * pairs directed edges go through CUB with an int item count
+  require(pairs < ((int64_t)1 << 30), "powerlaw_graph: too many edges");
   cudaStream_t st = ctx->stream;
   DevBuf w((size_t)n * 8, st), cdf((size_t)n * 8, st);
   k_weights<<<grid_for(ctx, n, 256), 256, 0, st>>>(n, 1.0 / (exponent - 1.0), w.as<double>());

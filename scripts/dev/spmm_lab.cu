@@ -342,6 +342,13 @@ int main(int argc, char** argv) {
     snprintf(nm, 64, "%s S=%d G=%d w=%d cta/sm=%d", TMA ? "tma.g4 " : "cp.async", S, G, WPB, CPS); \
     run(nm, [&] { k_ring<S, G, TMA><<<148 * CPS, WPB * 32, sm, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, map, (float4*)d_C); }, false); \
   }
+  VR(4, 4, false, 16, 1)
+  VR(3, 8, false, 8, 1)
+  VR(4, 4, true, 16, 1)
+  VR(4, 8, true, 8, 1)
+  VR(2, 8, true, 16, 1)
+  VR(6, 4, true, 16, 1)
+  VR(3, 4, true, 32, 1)
   // L2 persistence window on B with the V0 kernel
   {
     int maxp = 0;
