@@ -276,6 +276,12 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, int32_t h, const float* s, const float* d,
                        double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan);
+/* ... plus the per-row statistics (n_rows x 4h: s, max, 1/sum; NULL = none)
+ * that sgnn_gat_column_pass_stats rebuilds alpha from */
+int sgnn_gat_attention_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
+                          const int32_t* cols, int32_t h, const float* s, const float* d,
+                          double beta, float* alpha, uint8_t* mask, float* row_stats,
+                          sgnn_rowplan plan);
 /* spmm_semibatched + bias (kernels.hpp:219-254) */
 int sgnn_gat_aggregate(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
                        int32_t h, int32_t k, const float* alpha, const float* M,
@@ -288,6 +294,11 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
 int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
                               const float* alpha, const uint8_t* mask, const float* da,
                               double beta, float* dy, float* dS, sgnn_rowplan plan);
+/* ... plus dot = sum_e alpha dAlpha per row and head into row_stats[3h..4h) */
+int sgnn_gat_softmax_backward_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
+                                 const float* alpha, const uint8_t* mask, const float* da,
+                                 double beta, float* dy, float* dS, float* row_stats,
+                                 sgnn_rowplan plan);
 /* spmm_semibatched_transposed + edge_col_sums + add_scaled_rows (258-295,
  * 614-658) over a block of columns (rows / perm index gathered G / edges) */
 int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
@@ -295,6 +306,16 @@ int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
                          const float* G, const float* alpha, const float* dy, const float* dS,
                          const float* a_src, const float* a_dst, float* dD, float* dM,
                          sgnn_rowplan plan);
+/* The same column pass rebuilding alpha / dy per edge from the gathered row
+ * statistics and dAlpha = <dX'_i, M_j> (kernels.hpp:342-377, 427-588 restated
+ * per column): the row-partitioned layer all-gathers 4 n h statistics
+ * instead of 2 q' h edge values.  d_own, M_own, dS: the block's own rows. */
+int sgnn_gat_column_stats_supported(int32_t h, int32_t k);
+int sgnn_gat_column_pass_stats(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
+                               const int32_t* rows, int32_t h, int32_t k, const float* G,
+                               const float* row_stats, const float* d_own, const float* M_own,
+                               double beta, const float* dS, const float* a_src,
+                               const float* a_dst, float* dD, float* dM, sgnn_rowplan plan);
 /* column_sums + attention_param_grad (dense.hpp:272-282, kernels.hpp:592-611) */
 int sgnn_gat_param_grads(sgnn_ctx ctx, int32_t n_rows, int32_t h, int32_t k, const float* G,
                          const float* M, const float* dS, const float* dD, float* d_bias,

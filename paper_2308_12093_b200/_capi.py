@@ -110,9 +110,14 @@ _SIGS = {
     "sgnn_rowplan_create": (INT, [VP, I32, VP, PVP]),
     "sgnn_rowplan_destroy": (INT, [VP]),
     "sgnn_gat_attention": (INT, [VP, I32, VP, VP, I32, VP, VP, D, VP, VP, VP]),
+    "sgnn_gat_attention_ex": (INT, [VP, I32, VP, VP, I32, VP, VP, D, VP, VP, VP, VP]),
     "sgnn_gat_aggregate": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP, VP]),
     "sgnn_gat_sddmm": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP]),
     "sgnn_gat_softmax_backward": (INT, [VP, I32, VP, I32, VP, VP, VP, D, VP, VP, VP]),
+    "sgnn_gat_softmax_backward_ex": (INT, [VP, I32, VP, I32, VP, VP, VP, D, VP, VP, VP, VP]),
+    "sgnn_gat_column_stats_supported": (INT, [I32, I32]),
+    "sgnn_gat_column_pass_stats": (INT, [VP, I32, VP, VP, I32, I32, VP, VP, VP, VP, D, VP, VP,
+                                         VP, VP, VP, VP]),
     "sgnn_gat_column_pass": (INT, [VP, I32, VP, VP, VP, I32, I32, VP, VP, VP, VP, VP, VP, VP,
                                    VP, VP]),
     "sgnn_gat_param_grads": (INT, [VP, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP]),

@@ -1444,10 +1444,13 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 
 // edge_scores + leaky_relu_edges + edge_softmax (kernels.hpp:427-534):
 // alpha, mask edge-major (q_local x h) for the block's rows; s block-local,
-// d indexed by column id
-int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
-                       const int32_t* cols, int32_t h, const float* s, const float* d,
-                       double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan) {
+// d indexed by column id.  row_stats (optional, n_rows x 4h): s, max and
+// 1 / sum per row and head -- what sgnn_gat_column_pass_stats rebuilds alpha
+// from on the ranks that own the columns
+int sgnn_gat_attention_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
+                          const int32_t* cols, int32_t h, const float* s, const float* d,
+                          double beta, float* alpha, uint8_t* mask, float* row_stats,
+                          sgnn_rowplan plan) {
   SGNN_API_BEGIN
   require(beta > 0, "gat_forward: beta must be positive");
   require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
@@ -1455,15 +1458,22 @@ int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
   const LongRows* pl = plan_of(plan);
   HR_SWITCH(h, 1, (g2::k_gat_attn4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
                       n_rows, rowptr, cols, s, d, (float)beta, alpha, mask,
-                      pl ? kLongRow : 0x7fffffff)));
+                      pl ? kLongRow : 0x7fffffff, row_stats)));
   launched(ctx);
   if (pl) {
     HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pl->nlong, 256, 0, ctx->stream>>>(
                         pl->long_row.as<int32_t>(), rowptr, cols, s, d, (float)beta, alpha,
-                        mask)));
+                        mask, row_stats)));
     launched(ctx);
   }
   SGNN_API_END
+}
+
+int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
+                       const int32_t* cols, int32_t h, const float* s, const float* d,
+                       double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan) {
+  return sgnn_gat_attention_ex(ctx, n_rows, rowptr, cols, h, s, d, beta, alpha, mask, nullptr,
+                               plan);
 }
 
 // spmm_semibatched + bias (kernels.hpp:219-254): out rows of the block
@@ -1522,25 +1532,34 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
 }
 
 // edge_softmax_backward + leaky_relu_edges_backward + edge_row_sums
-// (kernels.hpp:481-495, 537-588)
-int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
-                              const float* alpha, const uint8_t* mask, const float* da,
-                              double beta, float* dy, float* dS, sgnn_rowplan plan) {
+// (kernels.hpp:481-495, 537-588).  row_stats (optional): the 4th slot of each
+// row gets dot = sum_e alpha dAlpha per head
+int sgnn_gat_softmax_backward_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
+                                 const float* alpha, const uint8_t* mask, const float* da,
+                                 double beta, float* dy, float* dS, float* row_stats,
+                                 sgnn_rowplan plan) {
   SGNN_API_BEGIN
   require(h == 1 || h == 2 || h == 4 || h == 8, "gat block: needs h in {1,2,4,8}");
   if (n_rows == 0) return SGNN_OK;
   const LongRows* pl = plan_of(plan);
   HR_SWITCH(h, 1, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n_rows), 256, 0, ctx->stream>>>(
                       n_rows, rowptr, alpha, mask, da, (float)beta, dy, dS,
-                      pl ? kLongRow : 0x7fffffff)));
+                      pl ? kLongRow : 0x7fffffff, row_stats)));
   launched(ctx);
   if (pl) {
     HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pl->nlong, 256, 0, ctx->stream>>>(
                         pl->long_row.as<int32_t>(), rowptr, alpha, mask, da, (float)beta, dy,
-                        dS)));
+                        dS, row_stats)));
     launched(ctx);
   }
   SGNN_API_END
+}
+
+int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
+                              const float* alpha, const uint8_t* mask, const float* da,
+                              double beta, float* dy, float* dS, sgnn_rowplan plan) {
+  return sgnn_gat_softmax_backward_ex(ctx, n_rows, rowptr, h, alpha, mask, da, beta, dy, dS,
+                                      nullptr, plan);
 }
 
 // spmm_semibatched_transposed + edge_col_sums + add_scaled_rows_inplace
@@ -1571,6 +1590,57 @@ int sgnn_gat_column_pass(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
     HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
                          pl->nseg, colptr, rows, perm, G4, alpha, dy, dS, as4, ad4, k, dD, dM4,
                          seg_args(*pl, part.as<float>(), ddp.as<float>()))));
+    launched(ctx);
+    HR_SWITCH(h, 1, (g2::k_gat_col_combine<HH><<<v2_grid(pl->nlong), 256, 0, ctx->stream>>>(
+                        pl->nlong, pl->long_row.as<int32_t>(), pl->long_first.as<int32_t>(),
+                        part.as<float4>(), ddp.as<float>(), dS, as4, ad4, k, dD, dM4)));
+    launched(ctx);
+  }
+  SGNN_API_END
+}
+
+// 1 when sgnn_gat_column_pass_stats supports (h, k): the v2 shapes whose
+// head dot reduces by xor (k/4 a power of two <= 32, or 32C with whole heads
+// per lane group)
+int sgnn_gat_column_stats_supported(int32_t h, int32_t k) {
+  const int R2 = v2_R<float>(h, k);
+  return R2 != 0 && R2 != 3 && sddmm_mode(k / 4, R2) != 0 ? 1 : 0;
+}
+
+// The column pass of a row-partitioned layer from per-row statistics (see
+// g2::k_gat_col3): rows index the gathered dX' (G) and the gathered row_stats
+// (4h per row: s, max, 1/sum, dot); d_own / M_own / dS are the block's own
+// rows (= its columns).  Replaces shipping alpha and dy (2 q' h values) with
+// 4 n h statistics.
+int sgnn_gat_column_pass_stats(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,
+                               const int32_t* rows, int32_t h, int32_t k, const float* G,
+                               const float* row_stats, const float* d_own, const float* M_own,
+                               double beta, const float* dS, const float* a_src,
+                               const float* a_dst, float* dD, float* dM, sgnn_rowplan plan) {
+  SGNN_API_BEGIN
+  block_check(h, k);
+  require(sgnn_gat_column_stats_supported(h, k), "gat block: column statistics need k/4 a power of two <= 32 or a multiple of 32");
+  if (n_cols == 0) return SGNN_OK;
+  const int R2 = v2_R<float>(h, k);
+  const LongRows* pl = plan_of(plan);
+  const unsigned wn = v2_windows<float>(h, k);
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  const float4* M4 = reinterpret_cast<const float4*>(M_own);
+  const float4* as4 = reinterpret_cast<const float4*>(a_src);
+  const float4* ad4 = reinterpret_cast<const float4*>(a_dst);
+  float4* dM4 = reinterpret_cast<float4*>(dM);
+  const float b = (float)beta;
+  g2::SegArgs sk;
+  sk.longest = pl ? kLongRow : 0x7fffffff;
+  HR_SWITCH(h, R2, (g2::k_gat_col3<HH, RR><<<dim3(v2_grid(n_cols), wn), 256, 0, ctx->stream>>>(
+                       n_cols, colptr, rows, G4, row_stats, d_own, M4, b, dS, as4, ad4, k, dD,
+                       dM4, sk)));
+  launched(ctx);
+  if (pl) {
+    DevBuf part((size_t)pl->nseg * h * k * 4, ctx->stream), ddp((size_t)pl->nseg * h * 4, ctx->stream);
+    HR_SWITCH(h, R2, (g2::k_gat_col3<HH, RR, true><<<dim3(v2_grid(pl->nseg), wn), 256, 0, ctx->stream>>>(
+                         pl->nseg, colptr, rows, G4, row_stats, d_own, M4, b, dS, as4, ad4, k,
+                         dD, dM4, seg_args(*pl, part.as<float>(), ddp.as<float>()))));
     launched(ctx);
     HR_SWITCH(h, 1, (g2::k_gat_col_combine<HH><<<v2_grid(pl->nlong), 256, 0, ctx->stream>>>(
                         pl->nlong, pl->long_row.as<int32_t>(), pl->long_first.as<int32_t>(),

@@ -783,6 +783,139 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 }
 
 // ---------------------------------------------------------------------------
+// Column pass of the row-partitioned layer (dist.DistGatLayer) that rebuilds
+// the per-edge values from per-row statistics instead of reading alpha / dy
+// (all-gather 4 n h row statistics, not 2 q' h edge values).
+// Row statistics, [row][4][H]: s (node score), max and 1 / sum of the softmax
+// (k_gat_attn4 / k_gat_attn_long), and dot = sum_e alpha dAlpha
+// (k_gat_sbwd4 / k_gat_sbwd_long).  Per edge (row i, column j):
+//   y = s_i + d_j, alpha = exp(lrelu(y) - max_i) * inv_i      (= k_gat_attn4)
+//   dAlpha = <dX'_i, M_j> per head                            (kernels.hpp:342-377)
+//   dy = alpha (dAlpha - dot_i), times beta where y <= 0      (= k_gat_sbwd4)
+// and then exactly what k_gat_col2 accumulates.  dX'_i is the row the column
+// pass gathers anyway and M_j is the column's own row, so rebuilding dAlpha
+// costs shuffles, not bytes.  Head reductions: L = k/4 <= 32 a power of two
+// (xor over the head's lanes) or L = 32C with R % C == 0 (chunks folded in
+// registers, then xor over the warp).  Every lane of a head ends with the
+// head's dAlpha, so dD needs no reduction (as in k_gat_col2).
+// ---------------------------------------------------------------------------
+template <int H, int R, bool SEG = false>
+__global__ void __launch_bounds__(256, R >= 8 ? 1 : (R >= 3 ? 2 : (R == 2 ? 3 : 4))) k_gat_col3(
+    int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
+    const float4* __restrict__ G, const float* __restrict__ stats, const float* __restrict__ dloc,
+    const float4* __restrict__ Mloc, float beta, const float* __restrict__ dS,
+    const float4* __restrict__ a_src, const float4* __restrict__ a_dst, int32_t k,
+    float* __restrict__ dD, float4* __restrict__ dM, SegArgs sg = {}) {
+  constexpr int U = R >= 4 ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int vo = blockIdx.y * 32 * R;
+  const int32_t q = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  if (q >= n) return;
+  const int fv = H * k / 4, L = k / 4;
+  int32_t beg, end, j = q;
+  if (SEG) {
+    beg = __ldg(sg.beg + q);
+    end = __ldg(sg.end + q);
+    j = __ldg(sg.row + q);
+  } else {
+    beg = __ldg(colptr + q);
+    end = __ldg(colptr + q + 1);
+    if (end - beg > sg.longest) return;
+  }
+  // heads of C whole chunks (L = 32C): fold the C chunk partials of a head
+  const int C = L > 32 ? L >> 5 : 1;
+  const int red = L > 32 ? 32 : L;  // lanes the head dot is xor-reduced over
+  int tr[R];
+  float4 acc[R], mj[R];
+  float dd[R], dj[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int v = vo + r * 32 + lane;
+    tr[r] = min(H - 1, v / L);
+    acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    dd[r] = 0.f;
+    mj[r] = v < fv ? __ldg(Mloc + (int64_t)j * fv + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    dj[r] = __ldg(dloc + (int64_t)j * H + tr[r]);
+  }
+  for (int32_t p = beg; p < end; p += U) {
+    uint32_t row[U];
+    float4 x[U][R];
+    float pd[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) row[u] = (uint32_t)__ldg(crows + min(p + u, end - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t v = vo + r * 32 + lane;
+        x[u][r] = v < (uint32_t)fv ? __ldg(G + row[u] * (uint32_t)fv + v)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        pd[u][r] = dot4(x[u][r], mj[r]);
+      }
+    // per-head dAlpha on every lane of the head
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (C > 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r % C == 0) {
+            float a = 0.f;
+#pragma unroll
+            for (int c = 0; c < R; ++c)
+              if (c < C && r + c < R) a += pd[u][r + c];
+            pd[u][r] = a;
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r % C == 0)
+          for (int o = red >> 1; o > 0; o >>= 1)
+            pd[u][r] += __shfl_xor_sync(0xffffffffu, pd[u][r], o);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (p + u >= end) break;
+      const float* st = stats + (int64_t)row[u] * (4 * H);
+      float a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r % C == 0) {  // first chunk of its head: alpha and dy of (edge, head)
+          const int t = tr[r];
+          const float y = __ldg(st + t) + dj[r];
+          a[r] = expf(lrelu(y, beta) - __ldg(st + H + t)) * __ldg(st + 2 * H + t);
+          const float dw = a[r] * (pd[u][r] - __ldg(st + 3 * H + t));
+          dd[r] += y > 0.f ? dw : beta * dw;
+        } else {
+          a[r] = a[r - 1];
+        }
+        if (vo + r * 32 + lane < fv) fma4(acc[r], a[r], x[u][r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r)
+    if (r % C != 0) dd[r] = dd[r - 1];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int v = vo + r * 32 + lane;
+    if (v < fv) {
+      if (SEG) {
+        sg.part[(int64_t)q * fv + v] = acc[r];
+        if (v % L == 0) sg.ddpart[(int64_t)q * H + tr[r]] = dd[r];
+        continue;
+      }
+      if (v % L == 0) dD[(int64_t)j * H + tr[r]] = dd[r];
+      const float cs = __ldg(dS + (int64_t)j * H + tr[r]);
+      const float4 as = __ldg(a_src + v), ad = __ldg(a_dst + v);
+      float4 o = acc[r];
+      fma4(o, cs, as);
+      fma4(o, dd[r], ad);
+      __stcs(dM + (int64_t)j * fv + v, o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // backward, part 4: the three column-sum gradients in one pass over the rows
 // (dense.hpp:272-282 column_sums for d_bias = 1^T dX'; kernels.hpp:592-611
 // attention_param_grad for d_a_src = sum_i dS[i,t] M[i,t,:] and d_a_dst with
@@ -917,7 +1050,8 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
                                                    const float* __restrict__ d, float beta,
                                                    float* __restrict__ alpha,
                                                    uint8_t* __restrict__ mask,
-                                                   int32_t longest = 0x7fffffff) {
+                                                   int32_t longest = 0x7fffffff,
+                                                   float* __restrict__ stats = nullptr) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
@@ -970,6 +1104,11 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
   group_allreduce<H>(sm, gl, OpSum());
 #pragma unroll
   for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
+  if (stats && gl == 0 && deg > 0) {  // row statistics for k_gat_col3: s, max, 1 / sum
+    st_heads<H>(stats + (int64_t)i * 4 * H, si);
+    st_heads<H>(stats + (int64_t)i * 4 * H + H, mx);
+    st_heads<H>(stats + (int64_t)i * 4 * H + 2 * H, sm);
+  }
   for (int32_t off = 0; off < wdeg; off += GS) {  // alpha, mask
     const int32_t e = beg + off + gl;
     if (off + gl < deg) {
@@ -1002,7 +1141,8 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
                                                    const float* __restrict__ da, float beta,
                                                    float* __restrict__ dy,
                                                    float* __restrict__ dS,
-                                                   int32_t longest = 0x7fffffff) {
+                                                   int32_t longest = 0x7fffffff,
+                                                   float* __restrict__ stats = nullptr) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
   const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
@@ -1035,6 +1175,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     }
   }
   group_allreduce<H>(dot, gl, OpSum());
+  if (stats && gl == 0 && deg > 0) st_heads<H>(stats + (int64_t)i * 4 * H + 3 * H, dot);
   const bool one = wdeg <= GS;  // a[], g[] still hold the lane's edge
   for (int32_t off = 0; off < wdeg; off += GS) {
     const int32_t e = beg + off + gl;
@@ -1120,7 +1261,8 @@ __global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict
                                                        const float* __restrict__ s,
                                                        const float* __restrict__ d, float beta,
                                                        float* __restrict__ alpha,
-                                                       uint8_t* __restrict__ mask) {
+                                                       uint8_t* __restrict__ mask,
+                                                       float* __restrict__ stats = nullptr) {
   __shared__ float sh[WPB][H];
   const int32_t i = __ldg(long_row + blockIdx.x);
   const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
@@ -1147,6 +1289,11 @@ __global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict
   block_allreduce<H>(sm, sh, OpSum());
 #pragma unroll
   for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
+  if (stats && threadIdx.x == 0) {
+    st_heads<H>(stats + (int64_t)i * 4 * H, si);
+    st_heads<H>(stats + (int64_t)i * 4 * H + H, mx);
+    st_heads<H>(stats + (int64_t)i * 4 * H + 2 * H, sm);
+  }
   for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
     float dj[H], a[H];
     ld_heads<H>(d + (int64_t)__ldg(cols + e) * H, dj);
@@ -1171,7 +1318,8 @@ __global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict
                                                        const uint8_t* __restrict__ mask,
                                                        const float* __restrict__ da, float beta,
                                                        float* __restrict__ dy,
-                                                       float* __restrict__ dS) {
+                                                       float* __restrict__ dS,
+                                                       float* __restrict__ stats = nullptr) {
   __shared__ float sh[WPB][H];
   const int32_t i = __ldg(long_row + blockIdx.x);
   const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
@@ -1186,6 +1334,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict
     for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
   }
   block_allreduce<H>(dot, sh, OpSum());
+  if (stats && threadIdx.x == 0) st_heads<H>(stats + (int64_t)i * 4 * H + 3 * H, dot);
   for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
     float a[H], g[H], y[H];
     ld_heads<H>(alpha + (int64_t)e * H, a);

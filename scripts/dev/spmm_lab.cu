@@ -238,6 +238,8 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+static bool g_reset = false;
+
 int main(int argc, char** argv) {
   const int n = 169343;
   const double deg = 1335587.0 / n;
@@ -314,6 +316,7 @@ int main(int argc, char** argv) {
     float tot = 0.f, best = 1e9f;
     const int reps = 20;
     for (int r = 0; r < reps; ++r) {
+      if (g_reset) CK(cudaCtxResetPersistingL2Cache());  // persisting lines -> normal
       CK(cudaMemsetAsync(flush, r, 256 << 20, st));
       cudaEventRecord(a, st);
       launch();
@@ -335,7 +338,7 @@ int main(int argc, char** argv) {
   run("v0 U=1 minB=8", [&] { k_v0<1, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
 
 #define VR(S, G, TMA, WPB, CPS)                                                                \
-  {                                                                                            \
+  if (argc > 1) {                                                                                            \
     const int sm = WPB * S * G * 512;                                                          \
     CK(cudaFuncSetAttribute(k_ring<S, G, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
     char nm[64];                                                                               \
@@ -348,7 +351,10 @@ int main(int argc, char** argv) {
   VR(4, 8, true, 8, 1)
   VR(2, 8, true, 16, 1)
   VR(6, 4, true, 16, 1)
-  VR(3, 4, true, 32, 1)
+  VR(4, 4, true, 8, 3)
+  VR(2, 4, true, 8, 6)
+  VR(4, 4, false, 8, 3)
+  VR(2, 4, false, 8, 6)
   // L2 persistence window on B with the V0 kernel
   {
     int maxp = 0;
@@ -362,7 +368,8 @@ int main(int argc, char** argv) {
     at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at));
-    for (float hr : {0.3f, 0.5f, 0.7f, 0.85f, 0.956f, 1.0f}) {
+    g_reset = true;  // honest flush: the previous iteration's persisting lines are evictable
+    for (float hr : {0.5f, 0.7f, 0.85f, 0.956f, 1.0f}) {
       at.accessPolicyWindow.hitRatio = hr;
       CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &at));
       char nm[64];

@@ -1,5 +1,5 @@
-"""Row-partitioned GCN layer with world_size 2 over gloo on the
-CPU.  The partition / all-gather / all-reduce logic of
+"""Row-partitioned GCN / GAT layers and 2-layer models with
+world_size 2..4 over gloo on the CPU.  The partition / all-gather / all-reduce logic of
 paper_2308_12093_b200.dist runs unchanged; the per-rank compute backend is a
 small CPU implementation injected by the test (the product backend is
 libsgnn_cuda.so).  Every rank's row block of the outputs and gradients is
@@ -13,47 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-
-class CpuOps:
-    """Test-only backend: CSR SpMM in stored order, numpy GEMMs, float64."""
-
-    class Adj:
-        def __init__(self, n_rows, rows, cols, vals):
-            self.rowptr = np.zeros(n_rows + 1, np.int64)
-            np.add.at(self.rowptr, np.asarray(rows, np.int64) + 1, 1)
-            self.rowptr = np.cumsum(self.rowptr)
-            self.cols, self.vals = np.asarray(cols), np.asarray(vals, np.float64)
-
-    def adjacency(self, n_rows, n_cols, rows, cols, vals, dtype):
-        return CpuOps.Adj(n_rows, rows, cols, vals)
-
-    def spmm(self, adj, B, bias=None):
-        B = B.numpy()
-        out = np.zeros((len(adj.rowptr) - 1, B.shape[1]))
-        for i in range(len(adj.rowptr) - 1):
-            for e in range(adj.rowptr[i], adj.rowptr[i + 1]):
-                out[i] += adj.vals[e] * B[adj.cols[e]]
-        t = torch.from_numpy(out)
-        return t if bias is None else t + bias
-
-    def empty(self, rows, cols, dtype):
-        return torch.empty((rows, cols), dtype=dtype)
-
-    def gemm(self, A, B, ta=False, tb=False, bias=None, out=None, colsum_b=None):
-        a = A.T if ta else A
-        b = B.T if tb else B
-        r = a @ b
-        if bias is not None:
-            r = r + bias
-        if colsum_b is not None:
-            colsum_b.copy_(B.sum(0))
-        if out is None:
-            return r
-        out.copy_(r)
-        return out
-
-    def colsum(self, X):
-        return X.sum(0)
+from _cpu_ops import CpuOps
 
 
 def _free_port():
@@ -169,3 +129,127 @@ def test_gat_blocks_reproduce_the_csc_view():
                 for q, r in zip(b["perm"][lo:hi], want):
                     e = canon[int(q)]
                     assert rows[e] == r and cols[e] == j
+
+
+# ---------------------------------------------------------------------------
+# partitioned GAT layer and the 2-layer models
+# ---------------------------------------------------------------------------
+def _gat_worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path.insert(0, root)
+        sys.path.insert(0, os.path.join(root, "oracle"))
+        import oracle as orc
+        from _cpu_ops import GatCpuOps
+        from paper_2308_12093_b200 import dist as pd
+
+        kind, n, m, h, k, exchange, fg = case
+        _, s, t = orc.synthetic_graph(n, 6.0, 5)
+        pat = orc.gat_pattern(n, s, t)
+        ops = GatCpuOps()
+        T = torch.from_numpy
+        if kind == "layer":
+            layer = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, k, ops, exchange=exchange)
+            r0, r1 = layer.r0, layer.r1
+            th, a_s, a_d, b = orc.gat_params(m, h, k, 21)
+            X = orc.random_uniform(n, m, 11)
+            G = orc.random_uniform(n, h * k, 12)
+            out, cache = layer.forward(T(X[r0:r1]), T(th), T(a_s), T(a_d), T(b))
+            grads = layer.backward(T(G[r0:r1]), T(th), T(a_s), T(a_d), cache, fg)
+            ref_o = orc.gat_forward(pat, X, th, a_s, a_d, b, h, 0.2)
+            ref_g = orc.gat_backward(pat, G, X, th, a_s, a_d, h, 0.2, fg)
+            errs = [orc.max_rel_diff(out.numpy(), ref_o[r0:r1])]
+            errs += [orc.max_rel_diff(g.numpy(), r) for g, r in zip(grads[:4], ref_g[:4])]
+            if fg:
+                errs.append(orc.max_rel_diff(grads[4].numpy(), ref_g[4][r0:r1]))
+            q.put((rank, max(errs), r1 - r0, layer.exchange))
+        elif kind == "gat2":
+            hid, o = k, 3
+            l1 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, hid, ops, exchange=exchange)
+            l2 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, o, ops, exchange=exchange)
+            prm = orc.gat2_params(m, h, hid, o, 7)
+            model = pd.DistGat2(l1, l2, m, hid, o, h, 7, input_grad=fg,
+                                params=[T(p) for p in prm])
+            r0, r1 = l1.r0, l1.r1
+            X = orc.random_uniform(n, m, 18)
+            tgt = orc.random_uniform(n, h * o, 19)
+            loss, out, grads, dx = model.train_step(T(X[r0:r1]), T(tgt[r0:r1]))
+            rl, rout, rgrads, rdx = orc.gat2_step(pat, X, prm, h, tgt, 0.2, fg)
+            errs = [abs(float(loss) - rl) / max(1.0, abs(rl)),
+                    orc.max_rel_diff(out.numpy(), rout[r0:r1])]
+            errs += [orc.max_rel_diff(g.numpy(), r) for g, r in zip(grads, rgrads)]
+            if fg:
+                errs.append(orc.max_rel_diff(dx.numpy(), rdx[r0:r1]))
+            q.put((rank, max(errs), r1 - r0, exchange))
+        else:  # gcn2
+            op = orc.gcn_operator(n, s, t)
+            layer = pd.DistGcnLayer(n, op.rows, op.cols, op.vals, ops, torch.float64)
+            hid, o = k, 4
+            prm = orc.gcn2_params(m, hid, o, 9)
+            model = pd.DistGcn2(layer, m, hid, o, 9, caching=True, input_grad=fg,
+                                params=[T(p) for p in prm])
+            r0, r1 = layer.r0, layer.r1
+            X = orc.random_uniform(n, m, 20)
+            tgt = orc.random_uniform(n, o, 21)
+            loss, out, grads, dx = model.train_step(T(X[r0:r1]), T(tgt[r0:r1]))
+            rl, rout, rgrads, rdx = orc.gcn2_step(op, X, prm, tgt, 0, True, fg)
+            errs = [abs(float(loss) - rl) / max(1.0, abs(rl)),
+                    orc.max_rel_diff(out.numpy(), rout[r0:r1])]
+            errs += [orc.max_rel_diff(g.numpy(), r) for g, r in zip(grads, rgrads)]
+            if fg:
+                errs.append(orc.max_rel_diff(dx.numpy(), rdx[r0:r1]))
+            q.put((rank, max(errs), r1 - r0, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gat_worker, args=(r, world, port, case, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sum(r[2] for r in results) == n
+    return results
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("exchange", ["stats", "edges"])
+@pytest.mark.parametrize("h,k", [(4, 3), (2, 5)])
+def test_row_partitioned_gat_layer(world, exchange, h, k):
+    """DistGatLayer over gloo: each rank's rows of out / dX and the
+    all-reduced dTheta, dA_src, dA_dst, db against the single-process oracle,
+    shipping either per-row statistics (alpha / dy rebuilt in the column pass)
+    or the edge values."""
+    n = 90
+    for rank, err, _, ex in _run(world, ("layer", n, 6, h, k, exchange, True), n):
+        assert ex == exchange
+        assert err < 1e-12, (rank, err)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_gat2_step(world):
+    """DistGat2 (Gat2Model over the partition: GAT -> ELU -> GAT, MSE) against
+    the oracle's Gat2Model step (pinned to the reference's)."""
+    n = 80
+    for rank, err, _, _ in _run(world, ("gat2", n, 5, 2, 3, "stats", True), n):
+        assert err < 1e-12, (rank, err)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_row_partitioned_gcn2_step(world):
+    """DistGcn2 against the oracle's Gcn2Model step (pinned to the reference's)."""
+    n = 100
+    for rank, err, _, _ in _run(world, ("gcn2", n, 6, 1, 5, None, True), n):
+        assert err < 1e-12, (rank, err)

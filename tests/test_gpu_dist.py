@@ -147,17 +147,22 @@ def test_activation_and_loss_entry_points(orc):
     assert abs(float(loss) - rl) < 1e-12 and orc.max_rel_diff(grad.cpu().numpy(), rg) < 1e-15
 
 
-@pytest.mark.parametrize("h,k", [(8, 32), (4, 12), (2, 64)])
-def test_dist_gat_layer_world1(nccl_world1, orc, h, k):
-    """Partitioned GAT layer (world 1): identical kernels in the same order as
-    the single-GPU layer (bit-identical results) and the oracle at 1e-4."""
+@pytest.mark.parametrize("h,k,exchange", [(8, 32, "edges"), (4, 12, "edges"), (2, 64, "edges"),
+                                          (8, 32, "stats"), (4, 16, "stats"), (2, 256, "stats"),
+                                          (1, 512, "stats")])
+def test_dist_gat_layer_world1(nccl_world1, orc, h, k, exchange):
+    """Partitioned GAT layer (world 1).  exchange="edges": the single-GPU
+    layer's kernels in the same order (bit-identical results).  "stats": the
+    column pass rebuilds alpha / dy from per-row statistics (alpha bit-identical,
+    dAlpha re-reduced), checked against the oracle at the north-star 1e-4."""
     from paper_2308_12093_b200 import device as d
     from paper_2308_12093_b200 import dist as pd
 
     n, m = 2200, 24
     _, s, t = orc.synthetic_graph(n, 8.0, 6)
     pat = orc.gat_pattern(n, s, t)
-    layer = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, k, "cuda:0")
+    layer = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, k, "cuda:0", exchange=exchange)
+    assert layer.exchange == exchange
     th, a_s, a_d, b = (torch.from_numpy(x.astype(np.float32)).cuda()
                        for x in orc.gat_params(m, h, k, 21))
     X = orc.random_uniform(n, m, 11)
@@ -170,15 +175,22 @@ def test_dist_gat_layer_world1(nccl_world1, orc, h, k):
     o1, c1 = d.gat_forward(P, Xc, th, a_s, a_d, b, h, 0.2, "full")
     g1 = d.gat_backward(P, Gc, th, a_s, a_d, c1, True)
     assert torch.equal(out, o1)
-    for a_, b_ in zip(grads, g1):
-        assert torch.equal(a_, b_)
+    if exchange == "edges":
+        for a_, b_ in zip(grads, g1):
+            assert torch.equal(a_, b_)
     ref_o = orc.gat_forward(pat, X, *orc.gat_params(m, h, k, 21), h, 0.2)
     assert orc.max_rel_diff(out.double().cpu().numpy(), ref_o) < 1e-4
+    ref_g = orc.gat_backward(pat, G, X, *orc.gat_params(m, h, k, 21)[:3], h, 0.2, True)
+    for g, r in zip(grads, ref_g):
+        assert orc.max_rel_diff(g.double().cpu().numpy(), r) < 1e-4
 
 
-def test_dist_gat_layer_world1_hub_rows(nccl_world1, orc):
-    """The partitioned GAT layer on a power-law graph (hub rows run through the
-    block entry points' row plans): bit-identical to the single-GPU layer."""
+@pytest.mark.parametrize("exchange", ["edges", "stats"])
+def test_dist_gat_layer_world1_hub_rows(nccl_world1, orc, exchange):
+    """The partitioned GAT layer on a power-law graph (hub rows / columns run
+    through the block entry points' row plans): forward bit-identical to the
+    single-GPU layer, gradients bit-identical ("edges") or within the fp32
+    bar of it ("stats")."""
     from paper_2308_12093_b200 import device as d
     from paper_2308_12093_b200 import dist as pd
 
@@ -187,8 +199,7 @@ def test_dist_gat_layer_world1_hub_rows(nccl_world1, orc):
     P = d.Pattern.gat_pattern(n, s, t)
     pa = P.arrays()
     assert int(torch.diff(pa["rowptr"]).max()) > 500
-    layer = pd.DistGatLayer(n, pa["rowptr"].cpu().numpy(), pa["cols"].cpu().numpy(), h, k,
-                            "cuda:0")
+    layer = pd.DistGatLayer(n, pa["rowptr"], pa["cols"], h, k, "cuda:0", exchange=exchange)
     th, a_s, a_d, b = d.gat_params(m, h, k, 3)
     X = d.random_uniform(n, m, 1)
     G = d.random_uniform(n, h * k, 2)
@@ -198,4 +209,31 @@ def test_dist_gat_layer_world1_hub_rows(nccl_world1, orc):
     g1 = d.gat_backward(P, G, th, a_s, a_d, c1, True)
     assert torch.equal(out, o1)
     for x, y in zip(grads, g1):
-        assert torch.equal(x, y)
+        if exchange == "edges":
+            assert torch.equal(x, y)
+        else:
+            assert orc.max_rel_diff(x.double().cpu().numpy(), y.double().cpu().numpy()) < 1e-4
+
+
+def test_dist_gat2_matches_oracle_model(nccl_world1, orc):
+    """Partitioned 2-layer GAT step (world 1) against oracle.gat2_step, pinned
+    to the reference's Gat2Model step."""
+    from paper_2308_12093_b200 import dist as pd
+
+    n, m, h, hid, o, seed = 1400, 20, 4, 8, 4, 5
+    _, s, t = orc.synthetic_graph(n, 7.0, 2)
+    pat = orc.gat_pattern(n, s, t)
+    l1 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, hid, "cuda:0")
+    l2 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, o, "cuda:0")
+    assert l1.exchange == "stats" and l2.exchange == "stats"
+    model = pd.DistGat2(l1, l2, m, hid, o, h, seed)
+    X = orc.random_uniform(n, m, seed + 11)
+    tgt = orc.random_uniform(n, h * o, seed + 12)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()  # noqa: E731
+    loss, out, grads, _ = model.train_step(cu(X), cu(tgt))
+    prm = [p.double().cpu().numpy() for p in model.p]  # the device's float32 parameters
+    rl, rout, rgrads, _ = orc.gat2_step(pat, X, prm, h, tgt, 0.2, False)
+    assert abs(float(loss) - rl) <= 1e-4 * max(1.0, abs(rl))
+    assert orc.max_rel_diff(out.double().cpu().numpy(), rout) < 1e-4
+    for g, r in zip(grads, rgrads):
+        assert orc.max_rel_diff(g.double().cpu().numpy(), r) < 1e-4
