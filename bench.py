@@ -486,6 +486,13 @@ def run_ours(args):
     h2d = hX.numel() * 4 + hG.numel() * 4
     d2h = (h_out.numel() + h_dth.numel() + h_db.numel() + h_dx.numel()) * 4
 
+    large = None
+    if not args.no_large:
+        try:
+            large = large_graph_steps(args, ctx, world, max(3, min(args.steps, 5)))
+        except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+            large = {"unavailable": f"{type(ex).__name__}: {ex}"}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -537,12 +544,97 @@ def run_ours(args):
         "sddmm": sddmm_line,
         "gat_roofline": gat_roofline,
         "models": models,
+        "large_graph": large,
         "setup_s": round(setup_s, 2),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+    if dist.is_initialized():
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# config 5: row-partitioned 2-layer GCN / GAT steps on the large power-law
+# graph, through the partitioned engine (paper_2308_12093_b200.dist) at every
+# N, N = 1 included, so the edges/s of the scaling curve come from one engine
+# ---------------------------------------------------------------------------
+LARGE_N, LARGE_EDGES, LARGE_M = 2449029, 61859140, 100
+
+
+def large_graph_steps(args, ctx, world, steps):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_12093_b200 import device as d
+    from paper_2308_12093_b200 import dist as pd
+
+    dev = ctx.device
+    stream = torch.cuda.current_stream(dev)
+    if not dist.is_initialized():  # N = 1 without torchrun: a one-rank NCCL group
+        for key, val in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"),
+                         ("MASTER_PORT", "29534")):
+            os.environ.setdefault(key, val)
+        dist.init_process_group("nccl", device_id=dev)
+    n = LARGE_N
+    t0 = time.perf_counter()
+    src, dst = d.powerlaw_graph(n, LARGE_EDGES / n, 2.5, SEED, ctx)
+    ones = torch.ones(src.numel(), dtype=torch.float32, device=dev)
+    r, c, v = d.canonicalize(n, n, src, dst, ones, ctx)
+    r, c, v = d.gcn_normalize(n, r, c, v, ctx)
+    Pg = d.Pattern.gat_pattern(n, src, dst, ctx)
+    pa = Pg.arrays()
+    rowptr, cols = pa["rowptr"], pa["cols"]
+    del src, dst, ones
+    gl = pd.DistGcnLayer(n, r, c, v, pd.DeviceOps(dev), torch.float32)
+    nnz_gcn = int(r.numel())
+    del r, c, v
+    l1 = pd.DistGatLayer(n, rowptr, cols, 8, 32, dev)
+    l2 = pd.DistGatLayer(n, rowptr, cols, 8, 8, dev)
+    nnz_gat = int(Pg.nnz)
+    del Pg, pa, rowptr, cols
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    X = d.random_uniform(n, LARGE_M, SEED + 11, ctx=ctx)
+    out = {"graph": f"powerlaw_graph(n={n}, deg={LARGE_EDGES}/{n}, exponent=2.5, seed={SEED})",
+           "n": n, "nnz_gcn": nnz_gcn, "nnz_gat": nnz_gat, "m": LARGE_M,
+           "engine": "paper_2308_12093_b200.dist (row partition, NCCL all-gather / all-reduce)",
+           "n_gpus": world, "scaling": "strong", "setup_s": round(setup_s, 2)}
+    for name, layer, make, ow in (
+            ("gcn2", gl, lambda: pd.DistGcn2(gl, LARGE_M, 256, 47, SEED + 13, caching=True), 47),
+            ("gat2", l1, lambda: pd.DistGat2(l1, l2, LARGE_M, 32, 8, 8, SEED + 13), 64)):
+        model = make()
+        r0, r1 = layer.r0, layer.r1
+        Xl = X[r0:r1].contiguous()
+        tgt = d.random_uniform(n, ow, SEED + 12, ctx=ctx)[r0:r1].contiguous()
+        for _ in range(2):
+            model.train_step(Xl, tgt)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(steps):
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            model.train_step(Xl, tgt)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.mean(ms)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+        nnz = nnz_gcn if name == "gcn2" else nnz_gat
+        out[name] = {"ms": round(step_ms, 3), "edges_per_s": round(2 * nnz / (step_ms * 1e-3), 1),
+                     "edges_per_s_note": "2 layers x nnz per step / step time (whole job)"}
+        del model, tgt, Xl
+    out["gcn2"]["shape"] = f"{LARGE_M}-256-47 adaptive+caching, MSE"
+    out["gat2"]["shape"] = (f"{LARGE_M}-(8x32)-(8x8) h=8, exchange "
+                            f"{l1.exchange}/{l2.exchange}, MSE")
+    out["rows_per_rank"] = [gl.bounds[p + 1] - gl.bounds[p] for p in range(world)]
+    del gl, l1, l2, X
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours_dist(args):
@@ -686,6 +778,12 @@ def run_ours_dist(args):
     t = torch.tensor([sum(ems) / len(ems)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
+    large = None
+    if not args.no_large:
+        try:
+            large = large_graph_steps(args, ctx, world, max(3, min(args.steps, 5)))
+        except Exception as ex:  # noqa: BLE001 -- reported, not fatal
+            large = {"unavailable": f"{type(ex).__name__}: {ex}"}
     h2d = (hX.numel() + hG.numel()) * 4 * world
     d2h = (h_out.numel() + h_dx.numel()) * 4 * world + (h_dth.numel() + h_db.numel()) * 4
     if rank == 0:
@@ -704,11 +802,13 @@ def run_ours_dist(args):
             "roofline": None, "cpu_baseline": None,
             "gat_layer": {"ms": round(gat_ms, 4), "heads": GAT_H, "k": GAT_K,
                           "partition": "row blocks of the GAT pattern (all-gather M, d, dX', "
-                                       "alpha, dy)"},
+                                       "per-row softmax statistics)",
+                          "exchange": glayer.exchange},
             "models": {"gcn2": {"ms": round(gcn2_ms, 4),
                                 "shape": f"{M_IN}-{GCN2_HID}-{MODEL_OUT}", "caching": True}},
             "edges_per_s": round(int(r.numel()) / (mean_ms * 1e-3), 1),
             "rows_per_rank": [layer.bounds[p + 1] - layer.bounds[p] for p in range(world)],
+            "large_graph": large,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
@@ -727,6 +827,8 @@ def main():
                     help="skip the reference's CPU timing of the 2-layer model steps")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the post-timing parity check against the reference")
+    ap.add_argument("--no-large", action="store_true",
+                    help="skip the config-5 large-graph steps (partitioned engine)")
     ap.add_argument("--dist", action="store_true",
                     help="use the row-partitioned multi-GPU path even at WORLD_SIZE=1")
     args = ap.parse_args()

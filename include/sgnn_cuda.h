@@ -276,7 +276,7 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 int sgnn_gat_attention(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
                        const int32_t* cols, int32_t h, const float* s, const float* d,
                        double beta, float* alpha, uint8_t* mask, sgnn_rowplan plan);
-/* ... plus the per-row statistics (n_rows x 4h: s, max, 1/sum; NULL = none)
+/* ... plus the per-row statistics (n_rows x h x 4: s, max, 1/sum, [dot]; NULL = none)
  * that sgnn_gat_column_pass_stats rebuilds alpha from */
 int sgnn_gat_attention_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
                           const int32_t* cols, int32_t h, const float* s, const float* d,
@@ -294,7 +294,7 @@ int sgnn_gat_sddmm(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const in
 int sgnn_gat_softmax_backward(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
                               const float* alpha, const uint8_t* mask, const float* da,
                               double beta, float* dy, float* dS, sgnn_rowplan plan);
-/* ... plus dot = sum_e alpha dAlpha per row and head into row_stats[3h..4h) */
+/* ... plus dot = sum_e alpha dAlpha per row and head into row_stats[row][head][3] */
 int sgnn_gat_softmax_backward_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, int32_t h,
                                  const float* alpha, const uint8_t* mask, const float* da,
                                  double beta, float* dy, float* dS, float* row_stats,

@@ -1444,7 +1444,7 @@ int sgnn_gat_transform(sgnn_ctx ctx, const float* X, int32_t n_rows, int32_t m,
 
 // edge_scores + leaky_relu_edges + edge_softmax (kernels.hpp:427-534):
 // alpha, mask edge-major (q_local x h) for the block's rows; s block-local,
-// d indexed by column id.  row_stats (optional, n_rows x 4h): s, max and
+// d indexed by column id.  row_stats (optional, n_rows x h x 4): s, max and
 // 1 / sum per row and head -- what sgnn_gat_column_pass_stats rebuilds alpha
 // from on the ranks that own the columns
 int sgnn_gat_attention_ex(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr,
@@ -1609,7 +1609,7 @@ int sgnn_gat_column_stats_supported(int32_t h, int32_t k) {
 
 // The column pass of a row-partitioned layer from per-row statistics (see
 // g2::k_gat_col3): rows index the gathered dX' (G) and the gathered row_stats
-// (4h per row: s, max, 1/sum, dot); d_own / M_own / dS are the block's own
+// ([row][head][4]: s, max, 1/sum, dot); d_own / M_own / dS are the block's own
 // rows (= its columns).  Replaces shipping alpha and dy (2 q' h values) with
 // 4 n h statistics.
 int sgnn_gat_column_pass_stats(sgnn_ctx ctx, int32_t n_cols, const int32_t* colptr,

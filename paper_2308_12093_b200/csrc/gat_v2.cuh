@@ -133,6 +133,24 @@ __device__ __forceinline__ void st_heads(float* __restrict__ p, const float (&v)
   }
 }
 
+// per-row statistics of the partitioned column pass, [row][head][4] =
+// (s, max, 1 / sum, dot): one 16-byte load per (edge, head) in k_gat_col3
+template <int H>
+__device__ __forceinline__ void st_stats3(float* __restrict__ p, const float (&s)[H],
+                                          const float (&mx)[H], const float (&inv)[H]) {
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    p[4 * t] = s[t];
+    p[4 * t + 1] = mx[t];
+    p[4 * t + 2] = inv[t];
+  }
+}
+template <int H>
+__device__ __forceinline__ void st_stat(float* __restrict__ p, const float (&v)[H]) {
+#pragma unroll
+  for (int t = 0; t < H; ++t) p[4 * t] = v[t];
+}
+
 template <int H>
 __device__ __forceinline__ void st_mask(uint8_t* __restrict__ p, uint32_t bits) {
   if constexpr (H == 8) {
@@ -786,9 +804,9 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 // Column pass of the row-partitioned layer (dist.DistGatLayer) that rebuilds
 // the per-edge values from per-row statistics instead of reading alpha / dy
 // (all-gather 4 n h row statistics, not 2 q' h edge values).
-// Row statistics, [row][4][H]: s (node score), max and 1 / sum of the softmax
+// Row statistics, [row][H][4]: s (node score), max and 1 / sum of the softmax
 // (k_gat_attn4 / k_gat_attn_long), and dot = sum_e alpha dAlpha
-// (k_gat_sbwd4 / k_gat_sbwd_long).  Per edge (row i, column j):
+// (k_gat_sbwd4 / k_gat_sbwd_long) -- one 16-byte load per (edge, head).  Per edge (row i, column j):
 //   y = s_i + d_j, alpha = exp(lrelu(y) - max_i) * inv_i      (= k_gat_attn4)
 //   dAlpha = <dX'_i, M_j> per head                            (kernels.hpp:342-377)
 //   dy = alpha (dAlpha - dot_i), times beta where y <= 0      (= k_gat_sbwd4)
@@ -800,7 +818,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 // head's dAlpha, so dD needs no reduction (as in k_gat_col2).
 // ---------------------------------------------------------------------------
 template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R >= 8 ? 1 : (R >= 3 ? 2 : (R == 2 ? 3 : 4))) k_gat_col3(
+__global__ void __launch_bounds__(256, R >= 8 ? 1 : (R >= 3 ? 2 : 4)) k_gat_col3(
     int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
     const float4* __restrict__ G, const float* __restrict__ stats, const float* __restrict__ dloc,
     const float4* __restrict__ Mloc, float beta, const float* __restrict__ dS,
@@ -875,15 +893,15 @@ __global__ void __launch_bounds__(256, R >= 8 ? 1 : (R >= 3 ? 2 : (R == 2 ? 3 : 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (p + u >= end) break;
-      const float* st = stats + (int64_t)row[u] * (4 * H);
+      const float4* st = reinterpret_cast<const float4*>(stats) + (int64_t)row[u] * H;
       float a[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r % C == 0) {  // first chunk of its head: alpha and dy of (edge, head)
-          const int t = tr[r];
-          const float y = __ldg(st + t) + dj[r];
-          a[r] = expf(lrelu(y, beta) - __ldg(st + H + t)) * __ldg(st + 2 * H + t);
-          const float dw = a[r] * (pd[u][r] - __ldg(st + 3 * H + t));
+          const float4 q = __ldg(st + tr[r]);  // (s, max, 1 / sum, dot) of (row, head)
+          const float y = q.x + dj[r];
+          a[r] = expf(lrelu(y, beta) - q.y) * q.z;
+          const float dw = a[r] * (pd[u][r] - q.w);
           dd[r] += y > 0.f ? dw : beta * dw;
         } else {
           a[r] = a[r - 1];
@@ -1105,9 +1123,7 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
 #pragma unroll
   for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
   if (stats && gl == 0 && deg > 0) {  // row statistics for k_gat_col3: s, max, 1 / sum
-    st_heads<H>(stats + (int64_t)i * 4 * H, si);
-    st_heads<H>(stats + (int64_t)i * 4 * H + H, mx);
-    st_heads<H>(stats + (int64_t)i * 4 * H + 2 * H, sm);
+    st_stats3<H>(stats + (int64_t)i * 4 * H, si, mx, sm);
   }
   for (int32_t off = 0; off < wdeg; off += GS) {  // alpha, mask
     const int32_t e = beg + off + gl;
@@ -1175,7 +1191,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     }
   }
   group_allreduce<H>(dot, gl, OpSum());
-  if (stats && gl == 0 && deg > 0) st_heads<H>(stats + (int64_t)i * 4 * H + 3 * H, dot);
+  if (stats && gl == 0 && deg > 0) st_stat<H>(stats + (int64_t)i * 4 * H + 3, dot);
   const bool one = wdeg <= GS;  // a[], g[] still hold the lane's edge
   for (int32_t off = 0; off < wdeg; off += GS) {
     const int32_t e = beg + off + gl;
@@ -1290,9 +1306,7 @@ __global__ void __launch_bounds__(256) k_gat_attn_long(const int32_t* __restrict
 #pragma unroll
   for (int t = 0; t < H; ++t) sm[t] = 1.f / sm[t];
   if (stats && threadIdx.x == 0) {
-    st_heads<H>(stats + (int64_t)i * 4 * H, si);
-    st_heads<H>(stats + (int64_t)i * 4 * H + H, mx);
-    st_heads<H>(stats + (int64_t)i * 4 * H + 2 * H, sm);
+    st_stats3<H>(stats + (int64_t)i * 4 * H, si, mx, sm);
   }
   for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
     float dj[H], a[H];
@@ -1334,7 +1348,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict
     for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
   }
   block_allreduce<H>(dot, sh, OpSum());
-  if (stats && threadIdx.x == 0) st_heads<H>(stats + (int64_t)i * 4 * H + 3 * H, dot);
+  if (stats && threadIdx.x == 0) st_stat<H>(stats + (int64_t)i * 4 * H + 3, dot);
   for (int32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
     float a[H], g[H], y[H];
     ld_heads<H>(alpha + (int64_t)e * H, a);

@@ -127,8 +127,9 @@ class GatCpuOps(CpuOps):
             inv = 1.0 / ex.sum(0)
             a[es] = ex * inv
             mk[es] = (y > 0).astype(np.uint8)
-            if st is not None:
-                st[i, :h], st[i, h:2 * h], st[i, 2 * h:3 * h] = s[i], mx, inv
+            if st is not None:  # [row][head][4] = (s, max, 1 / sum, dot)
+                q = st[i].reshape(h, 4)
+                q[:, 0], q[:, 1], q[:, 2] = s[i], mx, inv
 
     def aggregate(self, nl, rowptr, cols, h, k, alpha, M, bias, out, plan):
         rp, cl, a = rowptr.numpy(), cols.numpy(), alpha.numpy()
@@ -159,7 +160,7 @@ class GatCpuOps(CpuOps):
             y[es] = np.where(mk[es] > 0, dw, beta * dw)
             ds[i] = y[es].sum(0)
             if st is not None:
-                st[i, 3 * h:] = dot
+                st[i].reshape(h, 4)[:, 3] = dot
 
     def _finish(self, j, h, k, acc, dd, dS, a_src, a_dst, dD, dM):
         dD.numpy()[j] = dd
@@ -184,7 +185,8 @@ class GatCpuOps(CpuOps):
         st, dj = stats.numpy(), d_own.numpy()
         for j in range(nl):
             r = rw[cp[j]:cp[j + 1]]
-            s, mx, inv, dot = (st[r, q * h:(q + 1) * h] for q in range(4))
+            q4 = st[r].reshape(len(r), h, 4)
+            s, mx, inv, dot = (q4[:, :, q] for q in range(4))
             y = s + dj[j][None]
             a = np.exp(_lrelu(y, beta) - mx) * inv
             dalpha = (G3[r] * M3[j][None]).sum(-1)

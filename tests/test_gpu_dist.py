@@ -223,8 +223,8 @@ def test_dist_gat2_matches_oracle_model(nccl_world1, orc):
     n, m, h, hid, o, seed = 1400, 20, 4, 8, 4, 5
     _, s, t = orc.synthetic_graph(n, 7.0, 2)
     pat = orc.gat_pattern(n, s, t)
-    l1 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, hid, "cuda:0")
-    l2 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, o, "cuda:0")
+    l1 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, hid, "cuda:0", exchange="stats")
+    l2 = pd.DistGatLayer(n, pat.rowptr, pat.cols, h, o, "cuda:0", exchange="stats")
     assert l1.exchange == "stats" and l2.exchange == "stats"
     model = pd.DistGat2(l1, l2, m, hid, o, h, seed)
     X = orc.random_uniform(n, m, seed + 11)
