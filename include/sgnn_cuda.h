@@ -95,6 +95,20 @@ const char* sgnn_last_error(void);
 const char* sgnn_version(void);
 /* stream: a cudaStream_t; NULL = the default stream (CUDA convention) */
 int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out);
+/* memtrack.hpp:19-94 MemTracker for the device engine: live / peak / total
+ * bytes per class (0 untracked, 1 transient, 2 cache, 3 output, 4 = all) of
+ * the layer intermediates, charged with their logical sizes (the reference's
+ * Array sizes); kernel scratch stays untracked.  Process-wide. */
+typedef enum {
+  SGNN_MEM_UNTRACKED = 0,
+  SGNN_MEM_TRANSIENT = 1,
+  SGNN_MEM_CACHE = 2,
+  SGNN_MEM_OUTPUT = 3,
+  SGNN_MEM_ALL = 4
+} sgnn_mem_class;
+int sgnn_mem_stats(int mem_class, int64_t* live, int64_t* peak, int64_t* total);
+/* peaks restart from the live level, totals from zero (memtrack.hpp:79-87) */
+int sgnn_mem_reset_peaks(void);
 int sgnn_ctx_destroy(sgnn_ctx ctx);
 int sgnn_ctx_set_stream(sgnn_ctx ctx, void* stream);
 int sgnn_ctx_synchronize(sgnn_ctx ctx);
@@ -238,6 +252,10 @@ int sgnn_gcn_backward(sgnn_ctx ctx, sgnn_adj adj, const void* d_out, const void*
 int sgnn_gcn_cache_destroy(sgnn_gcn_cache cache);
 /* gcn.hpp:72-75 retained_bytes */
 int sgnn_gcn_cache_retained_bytes(sgnn_gcn_cache cache, int64_t* out);
+/* gcn.hpp:66-76 GcnCache fields: device X (borrowed; uncached schemes) or the
+ * owned P = A'X (cached scheme); the absent one is NULL */
+int sgnn_gcn_cache_arrays(sgnn_gcn_cache cache, const void** saved_input,
+                          const void** saved_propagated);
 
 /* ---- GAT layer (gat.hpp:89-219) ------------------------------------------ */
 int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
@@ -251,6 +269,10 @@ int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const voi
 int sgnn_gat_cache_destroy(sgnn_gat_cache cache);
 /* gat.hpp:66-71 extra_bytes (== gat_cache_footprint at every level) */
 int sgnn_gat_cache_extra_bytes(sgnn_gat_cache cache, int64_t* out);
+/* gat.hpp:56-72 GatCache fields retained at the cache level (NULL otherwise):
+ * M (n x hk), s / d node scores (n x h), alpha / mask edge-major (q x h) */
+int sgnn_gat_cache_arrays(sgnn_gat_cache cache, const void** M, const void** s, const void** d,
+                          const void** alpha, const uint8_t** mask);
 /* cached (level full) or recomputed (gat.hpp:150-170) attention, converted to
  * the reference head-major layout: alpha (h x q, dtype), mask (h x q bytes) */
 int sgnn_gat_cache_edge_values(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache cache,

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -75,6 +76,25 @@ inline void launched(sgnn_ctx ctx) {
   if (e != cudaSuccess) throw cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
+// Device memory accounting by class (memtrack.hpp:19-94 MemTracker on the
+// device): live / peak / total bytes of the layer intermediates the reference
+// classifies as transient, cache or output.  Buffers are charged with their
+// LOGICAL size (what the reference's Array would hold: n x k scalars, 1-byte
+// masks) when a layer tags them; kernel scratch (split-K partials, hub-row
+// partials, sort temporaries) stays untracked like the reference's
+// untracked class.  Process-wide and mutex-protected, like the reference's.
+enum MemCls : int { kUntracked = 0, kTransient = 1, kCache = 2, kOutput = 3 };
+
+class MemTrack {
+ public:
+  static MemTrack& get();
+  void on_alloc(int c, size_t b);
+  void on_free(int c, size_t b);
+  void on_reclass(int from, int to, size_t b);
+  void stats(int c, int64_t* live, int64_t* peak, int64_t* total);  // c == 4: all classes
+  void reset_peaks();
+};
+
 // Stream-ordered device buffer (cudaMallocAsync from the pooled default mem
 // pool: transients cost no cudaMalloc/cudaFree round trips on the hot path).
 class DevBuf {
@@ -93,15 +113,33 @@ class DevBuf {
       p_ = o.p_;
       bytes_ = o.bytes_;
       stream_ = o.stream_;
+      cls_ = o.cls_;
+      charged_ = o.charged_;
       o.p_ = nullptr;
       o.bytes_ = 0;
+      o.charged_ = 0;
     }
     return *this;
   }
   void reset() {
+    if (charged_) MemTrack::get().on_free(cls_, charged_);
+    charged_ = 0;
     if (p_) cudaFreeAsync(p_, stream_);
     p_ = nullptr;
     bytes_ = 0;
+  }
+  // charge `logical` bytes of this buffer to class `cls` (memory accounting)
+  DevBuf& track(int cls, size_t logical) {
+    if (charged_) MemTrack::get().on_free(cls_, charged_);
+    cls_ = cls;
+    charged_ = logical;
+    if (charged_) MemTrack::get().on_alloc(cls_, charged_);
+    return *this;
+  }
+  // ScopedMemClass / Array::reclassify (memtrack.hpp:176-181)
+  void reclassify(int to) {
+    if (charged_ && to != cls_) MemTrack::get().on_reclass(cls_, to, charged_);
+    cls_ = to;
   }
   template <class T>
   T* as() const {
@@ -115,6 +153,8 @@ class DevBuf {
   void* p_ = nullptr;
   size_t bytes_ = 0;
   cudaStream_t stream_ = nullptr;
+  int cls_ = kUntracked;
+  size_t charged_ = 0;
 };
 
 inline size_t dtype_size(int dtype) {

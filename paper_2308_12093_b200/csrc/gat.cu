@@ -905,16 +905,25 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
     launch_fwd<T, false, true>(ctx, n, rp, ci, M.as<T>(), s.as<T>(), d.as<T>(), h, k, beta,
                                bias, out, nullptr, nullptr);
   }
-  // reclassify retained buffers into the cache (gat.hpp:123-137)
+  // reclassify retained buffers into the cache (gat.hpp:123-137); charged
+  // with the reference's sizes (cost.hpp:236-248 footprint)
   c->saved_input = X;
-  if (level >= SGNN_GAT_FEATURES) c->M = std::move(M);
+  c->q = q;
+  if (level >= SGNN_GAT_FEATURES) {
+    c->M = std::move(M);
+    c->M.track(kCache, (size_t)n * hk * sizeof(T));
+  }
   if (level == SGNN_GAT_NODE_ATTENTION) {
     c->s = std::move(s);
     c->d = std::move(d);
+    c->s.track(kCache, (size_t)n * h * sizeof(T));
+    c->d.track(kCache, (size_t)n * h * sizeof(T));
   }
   if (level == SGNN_GAT_FULL) {
     c->alpha = std::move(alpha);
     c->mask = std::move(mask);
+    c->alpha.track(kCache, (size_t)q * h * sizeof(T));
+    c->mask.track(kCache, (size_t)q * h);
   }
 }
 
@@ -1322,6 +1331,20 @@ int sgnn_gat_cache_destroy(sgnn_gat_cache c) {
   SGNN_API_END
 }
 
+// device arrays the cache retains (NULL where the level does not keep them):
+// M (n x hk), s / d (n x h), alpha / mask edge-major (q x h)
+int sgnn_gat_cache_arrays(sgnn_gat_cache c, const void** M, const void** s, const void** d,
+                          const void** alpha, const uint8_t** mask) {
+  SGNN_API_BEGIN
+  require(c != nullptr, "gat cache: null handle");
+  if (M) *M = c->M.get();
+  if (s) *s = c->s.get();
+  if (d) *d = c->d.get();
+  if (alpha) *alpha = c->alpha.get();
+  if (mask) *mask = c->mask.as<uint8_t>();
+  SGNN_API_END
+}
+
 int sgnn_gat_cache_extra_bytes(sgnn_gat_cache c, int64_t* out) {
   SGNN_API_BEGIN
   // gat.hpp:66-71: bytes owned beyond the retained input; buffers carry +8
@@ -1330,7 +1353,7 @@ int sgnn_gat_cache_extra_bytes(sgnn_gat_cache c, int64_t* out) {
   int64_t b = 0;
   if (c->M.get()) b += sb * c->n * c->h * c->k;
   if (c->s.get()) b += 2 * sb * c->n * c->h;
-  if (c->alpha.get()) b += (int64_t)(c->alpha.bytes() - 8) + (int64_t)(c->mask.bytes() - 8);
+  if (c->alpha.get()) b += (sb + 1) * c->q * c->h;
   *out = b;
   SGNN_API_END
 }

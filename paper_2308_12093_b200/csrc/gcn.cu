@@ -46,12 +46,14 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
   const T* av = A->vals.as<T>();
   if (s.forward == SGNN_TRANSFORM_FIRST) {
     DevBuf M((size_t)n * k * sizeof(T), st);
+    M.track(kTransient, M.bytes());  // gcn.hpp:103-106
     gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
     spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz, fwd_plan(ctx, A));
     if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
     c->saved_input = X;
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
+    P.track(kTransient, P.bytes());  // gcn.hpp:114-117
     spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
     bool fused = false;
     if constexpr (sizeof(T) == 4)
@@ -61,8 +63,10 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
       gemm<T>(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias);
       if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
     }
-    if (s.forward == SGNN_PROPAGATE_FIRST_CACHED)
-      c->saved_propagated = std::move(P);  // reclassified into the cache (gcn.hpp:124)
+    if (s.forward == SGNN_PROPAGATE_FIRST_CACHED) {
+      P.reclassify(kCache);  // reclassified into the cache (gcn.hpp:124)
+      c->saved_propagated = std::move(P);
+    }
     else
       c->saved_input = X;
   }
@@ -91,6 +95,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     case SGNN_FUSED_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf S((size_t)n * k * sizeof(T), st);
+      S.track(kTransient, S.bytes());  // gcn.hpp:152-155
       column_sums<T>(ctx, G, n, k, d_bias);
       spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bwd_plan(ctx, A));
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
@@ -109,10 +114,12 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
     case SGNN_SPLIT_PROPAGATE: {
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf P((size_t)n * m * sizeof(T), st);
+      P.track(kTransient, P.bytes());  // gcn.hpp:163-167
       spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
       gemm_tn_colsum<T>(ctx, P.as<T>(), n, m, G, n, k, d_theta, d_bias);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
+        G2.track(kTransient, G2.bytes());
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
         spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
                     bwd_plan(ctx, A));
@@ -125,6 +132,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       gemm_tn_colsum<T>(ctx, P, n, m, G, n, k, d_theta, d_bias);
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
+        G2.track(kTransient, G2.bytes());  // gcn.hpp:180-184
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
         spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
                     bwd_plan(ctx, A));
@@ -218,6 +226,17 @@ extern "C" {
 int sgnn_gcn_cache_destroy(sgnn_gcn_cache c) {
   SGNN_API_BEGIN
   delete c;
+  SGNN_API_END
+}
+
+// device arrays the cache retains: the borrowed X (uncached schemes) or the
+// owned P = A'X (propagate_first_cached); the other is NULL
+int sgnn_gcn_cache_arrays(sgnn_gcn_cache c, const void** saved_input,
+                          const void** saved_propagated) {
+  SGNN_API_BEGIN
+  require(c != nullptr, "gcn cache: null handle");
+  if (saved_input) *saved_input = c->saved_propagated.get() ? nullptr : c->saved_input;
+  if (saved_propagated) *saved_propagated = c->saved_propagated.get();
   SGNN_API_END
 }
 

@@ -3,6 +3,7 @@
 // synthetic graph generator (graph.hpp).  No device work here except the
 // context's stream/pool setup.
 #include <algorithm>
+#include <mutex>
 #include <unordered_set>
 #include <vector>
 
@@ -12,6 +13,55 @@
 namespace sgnn {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& s) { g_last_error = s; }
+
+// ---- device memory accounting (memtrack.hpp:19-94) --------------------------
+namespace {
+struct MemCat {
+  int64_t live = 0, peak = 0, total = 0;
+};
+std::mutex g_mem_mu;
+MemCat g_mem[4], g_mem_all;
+}  // namespace
+
+MemTrack& MemTrack::get() {
+  static MemTrack t;
+  return t;
+}
+void MemTrack::on_alloc(int c, size_t b) {
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  for (MemCat* k : {&g_mem[c], &g_mem_all}) {
+    k->live += (int64_t)b;
+    k->total += (int64_t)b;
+    k->peak = std::max(k->peak, k->live);
+  }
+}
+void MemTrack::on_free(int c, size_t b) {
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  g_mem[c].live -= (int64_t)b;
+  g_mem_all.live -= (int64_t)b;
+}
+void MemTrack::on_reclass(int from, int to, size_t b) {
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  g_mem[from].live -= (int64_t)b;
+  MemCat& k = g_mem[to];
+  k.live += (int64_t)b;
+  k.total += (int64_t)b;
+  k.peak = std::max(k.peak, k.live);
+}
+void MemTrack::stats(int c, int64_t* live, int64_t* peak, int64_t* total) {
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  const MemCat& k = c == 4 ? g_mem_all : g_mem[c];
+  if (live) *live = k.live;
+  if (peak) *peak = k.peak;
+  if (total) *total = k.total;
+}
+void MemTrack::reset_peaks() {  // peaks restart from the live level (memtrack.hpp:79-87)
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  for (MemCat* k : {&g_mem[0], &g_mem[1], &g_mem[2], &g_mem[3], &g_mem_all}) {
+    k->peak = k->live;
+    k->total = 0;
+  }
+}
 }  // namespace sgnn
 
 using namespace sgnn;
@@ -20,6 +70,19 @@ extern "C" {
 
 const char* sgnn_last_error(void) { return g_last_error.c_str(); }
 const char* sgnn_version(void) { return "sgnn-b200 0.1 (sm_100a)"; }
+
+int sgnn_mem_stats(int mem_class, int64_t* live, int64_t* peak, int64_t* total) {
+  SGNN_API_BEGIN
+  require(mem_class >= 0 && mem_class <= 4, "sgnn_mem_stats: class must be 0..4");
+  MemTrack::get().stats(mem_class, live, peak, total);
+  SGNN_API_END
+}
+
+int sgnn_mem_reset_peaks(void) {
+  SGNN_API_BEGIN
+  MemTrack::get().reset_peaks();
+  SGNN_API_END
+}
 
 int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out) {
   SGNN_API_BEGIN

@@ -62,6 +62,7 @@ struct sgnn_gat_cache_s {
   int level = SGNN_GAT_NONE;
   int dtype = SGNN_F32;
   int32_t n = 0, m = 0, h = 0, k = 0;
+  int64_t q = 0;  // pattern nnz
   double beta = 0.2;
   const void* saved_input = nullptr;  // borrowed, always retained
   sgnn::DevBuf M;                     // level >= features

@@ -94,6 +94,23 @@ class Context:
             self.handle = None
 
 
+MEM_CLASSES = {"untracked": 0, "transient": 1, "cache": 2, "output": 3, "all": 4}
+
+
+def memory_stats(mem_class):
+    """(live, peak, total) device bytes of a class (memtrack.hpp:19-94 on the
+    device engine: layer intermediates charged with their logical sizes)."""
+    live, peak, total = C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib.sgnn_mem_stats(MEM_CLASSES[mem_class], C.byref(live), C.byref(peak),
+                             C.byref(total)))
+    return live.value, peak.value, total.value
+
+
+def reset_memory_peaks():
+    """Peaks restart from the live level (memtrack.hpp:79-87)."""
+    check(lib.sgnn_mem_reset_peaks())
+
+
 def _ctx(ctx):
     return ctx if ctx is not None else Context.default()
 
