@@ -13,6 +13,7 @@
 #include <memory>
 #include <optional>
 
+#include "sgnn/bench.hpp"
 #include "sgnn/cost.hpp"
 #include "sgnn/gat.hpp"
 #include "sgnn/gcn.hpp"
@@ -58,6 +59,47 @@ long long ref_synthetic_graph(int n, double deg, unsigned long long seed, int* s
     if (dst) dst[i] = g.edges[i].dst;
   }
   return static_cast<long long>(g.edges.size());
+}
+
+// bench.hpp run_benchmark (BenchReport, schema_version 1) of one
+// configuration with a minimal timing protocol (0 warmups, 1 block x 1 run):
+// the report JSON (report_to_json) is written into `out` (cap bytes).
+// Returns the JSON length, or -1 (text in ref_last_error()).
+long long ref_bench_report_json(const char* dataset, int gat2, int fmt, int hidden, int heads,
+                                int policy, int level, int fwdbwd, int fg, int f32,
+                                int in_features, int classes, unsigned long long seed,
+                                char* out, long long cap) {
+  try {
+    BenchConfig cfg;
+    cfg.dataset = dataset;
+    cfg.format = static_cast<SparseFormat>(fmt);
+    cfg.pass = fwdbwd ? BenchPass::forward_backward : BenchPass::forward;
+    cfg.warmups = 0;
+    cfg.blocks = 1;
+    cfg.runs_per_block = 1;
+    cfg.seed = seed;
+    cfg.f32 = f32 != 0;
+    ModelConfig& mc = cfg.model;
+    mc.kind = gat2 ? ModelKind::gat2 : ModelKind::gcn2;
+    mc.in_features = in_features;
+    mc.hidden = hidden;
+    mc.out_features = classes;
+    mc.heads = heads;
+    mc.scheme = static_cast<SchemePolicy>(policy);
+    mc.input_grad = fg != 0;
+    if (gat2) mc.gat_level = static_cast<GatCacheLevel>(level);
+    else mc.caching = level != 0;
+    const std::string js = report_to_json(run_benchmark(cfg)).dump();
+    if (static_cast<long long>(js.size()) + 1 > cap) {
+      g_err = "ref_bench_report_json: buffer too small";
+      return -1;
+    }
+    std::memcpy(out, js.c_str(), js.size() + 1);
+    return static_cast<long long>(js.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 // graph.hpp load_graph: returns the edge count (arrays filled when non-null,

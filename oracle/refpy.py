@@ -35,6 +35,8 @@ def load():
         "ref_synthetic_graph": (LL, [INT, D, ULL, VP, VP]),
         "ref_random_uniform": (None, [INT, INT, ULL, D, D, f64p]),
         "ref_load_graph": (LL, [C.c_char_p, INT, C.POINTER(INT), VP, VP, VP]),
+        "ref_bench_report_json": (LL, [C.c_char_p, INT, INT, INT, INT, INT, INT, INT, INT, INT,
+                                       INT, INT, ULL, C.c_char_p, LL]),
         "ref_coo_canonicalize": (LL, [INT, INT, LL, i32p, i32p, f64p, i32p, i32p, f64p]),
         "ref_gcn_normalize": (LL, [INT, LL, i32p, i32p, f64p, i32p, i32p, f64p]),
         "ref_gcn_normalize_f32": (LL, [INT, LL, i32p, i32p, f32p, i32p, i32p, f32p]),
