@@ -944,6 +944,80 @@ static bool tc_disabled() {
   return v == 1;
 }
 
+// Zero-padded copy of a rows x cols row-major matrix (pitch ld) into an
+// orows x ocols one: TMA needs 16-byte row pitches, so operands whose stored
+// width is not a multiple of 4 floats (Cora's 1433 input features) are staged
+// with zero columns (and zero K rows) -- the extra products are exact zeros.
+__global__ void k_pad2d(int32_t rows, int32_t cols, const float* __restrict__ src, int32_t ld,
+                        int32_t orows, int32_t ocols, float* __restrict__ dst) {
+  const int64_t total = (int64_t)orows * ocols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(i / ocols), c = (int32_t)(i % ocols);
+    dst[i] = (r < rows && c < cols) ? __ldg(src + (int64_t)r * ld + c) : 0.f;
+  }
+}
+
+static int32_t round4(int32_t x) { return (x + 3) & ~3; }
+
+bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
+                 int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
+                 float* colsum_b, const float* att_src, const float* att_dst, float* s_out,
+                 float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
+                 const float* elu_saved);
+
+// Operands with stored widths that are not multiples of 4: stage padded
+// copies (K padded with zeros on both operands, M / N padded as stored
+// widths), run the tcgen05 GEMM on them and copy the M x N block back.
+static bool gemm_tc_f32_padded(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca,
+                               const float* B, int32_t rb, int32_t cb, bool ta, bool tb,
+                               float* C, const float* bias, float* colsum_b,
+                               const float* att_src, const float* att_dst, float* s_out,
+                               float* d_out, int heads, uint8_t* relu_out,
+                               const uint8_t* mask_in, const float* elu_saved) {
+  const int32_t M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
+  const int32_t K4 = round4(K), M2 = ta ? round4(M) : M, N2 = tb ? N : round4(N);
+  const bool same_out = M2 == M && N2 == N;
+  if (!same_out && (att_src || relu_out || mask_in || elu_saved)) return false;
+  const int32_t ra2 = ta ? K4 : M, ca2 = ta ? M2 : K4, rb2 = tb ? N : K4, cb2 = tb ? K4 : N2;
+  cudaStream_t st = ctx->stream;
+  DevBuf a2((size_t)ra2 * ca2 * 4, st), b2((size_t)rb2 * cb2 * 4, st);
+  k_pad2d<<<grid_for(ctx, (int64_t)ra2 * ca2, 256), 256, 0, st>>>(ra, ca, A, ca, ra2, ca2,
+                                                                   a2.as<float>());
+  launched(ctx);
+  k_pad2d<<<grid_for(ctx, (int64_t)rb2 * cb2, 256), 256, 0, st>>>(rb, cb, B, cb, rb2, cb2,
+                                                                   b2.as<float>());
+  launched(ctx);
+  DevBuf c2, bias2, cs2;
+  float* Cp = C;
+  const float* bp = bias;
+  float* csp = colsum_b;
+  if (!same_out) {
+    c2 = DevBuf((size_t)M2 * N2 * 4, st);
+    Cp = c2.as<float>();
+    if (bias && N2 != N) {
+      bias2 = DevBuf((size_t)N2 * 4, st);
+      k_pad2d<<<1, 256, 0, st>>>(1, N, bias, N, 1, N2, bias2.as<float>());
+      launched(ctx);
+      bp = bias2.as<float>();
+    }
+    if (colsum_b && N2 != N) {
+      cs2 = DevBuf((size_t)N2 * 4, st);
+      csp = cs2.as<float>();
+    }
+  }
+  if (!gemm_tc_f32(ctx, a2.as<float>(), ra2, ca2, b2.as<float>(), rb2, cb2, ta, tb, Cp, bp, csp,
+                   att_src, att_dst, s_out, d_out, heads, relu_out, mask_in, elu_saved))
+    return false;
+  if (!same_out) {
+    SGNN_CUDA(cudaMemcpy2DAsync(C, (size_t)N * 4, Cp, (size_t)N2 * 4, (size_t)N * 4, M,
+                                cudaMemcpyDeviceToDevice, st));
+    if (colsum_b && csp != colsum_b)
+      SGNN_CUDA(cudaMemcpyAsync(colsum_b, csp, (size_t)N * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return true;
+}
+
 // Returns false (caller falls back to the SIMT kernel) when the shape or the
 // operand alignment does not fit the TMA/UMMA path.  colsum_b (optional, only
 // for C = A^T B with B read MN-major and split in the kernel): also writes the
@@ -960,7 +1034,9 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
   if (M <= 0 || N <= 0 || K <= 0) return false;
   if ((int64_t)M * N * K < (int64_t)1 << 20) return false;  // tiny: SIMT is fine
-  if ((ca & 3) || (cb & 3)) return false;                     // 16-byte row pitch for TMA
+  if ((ca & 3) || (cb & 3))  // 16-byte row pitches for TMA: stage padded operands
+    return gemm_tc_f32_padded(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, colsum_b, att_src,
+                              att_dst, s_out, d_out, heads, relu_out, mask_in, elu_saved);
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
   if ((reinterpret_cast<uintptr_t>(C) & 15) || (bias && (reinterpret_cast<uintptr_t>(bias) & 15)))
     return false;

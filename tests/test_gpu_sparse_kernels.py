@@ -153,9 +153,13 @@ def test_edge_softmax_requires_self_loops(d):
 
 
 # (20000, 256, 320): 160-wide tiles (two per row block), split-K dTheta shape;
-# (5000, 96, 300): 160-wide tiles with a ragged last tile
+# (5000, 96, 300): 160-wide tiles with a ragged last tile; stored widths that
+# are not multiples of 4 (Cora's 1433 features) run on tcgen05 from padded
+# staging copies: (2708, 1433, 16) pads K, (3000, 64, 1433) pads N (and K
+# with tb), (1433, 2708, 16) with ta pads M (the dTheta shape)
 @pytest.mark.parametrize("shape", [(1000, 7, 5), (300, 128, 256), (4096, 64, 40), (70000, 16, 8),
-                                   (20000, 256, 320), (5000, 96, 300)])
+                                   (20000, 256, 320), (5000, 96, 300), (2708, 1433, 16),
+                                   (3000, 64, 1433), (1433, 2708, 16)])
 @pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True)])
 def test_gemm_vs_oracle(d, orc, shape, trans):
     n, m, k = shape
@@ -222,3 +226,15 @@ def test_gat_transform_scores(d, orc, hk):
     assert orc.max_rel_diff(np_(M), Mr) < 1e-4
     assert orc.max_rel_diff(np_(s), sr) < 1e-4
     assert orc.max_rel_diff(np_(dd), dr) < 1e-4
+
+
+def test_unaligned_widths_run_on_tensor_cores(d, orc):
+    """Cora's X (2708 x 1433, fp32): the 5732-byte row pitch is staged into
+    zero-padded copies for the TMA / tcgen05 GEMM (pad A, pad B, Theta hi/lo
+    split, GEMM) instead of the one-launch SIMT fallback."""
+    A = cu(orc.random_uniform(2708, 1433, 1).astype(np.float32))
+    B = cu(orc.random_uniform(1433, 16, 2).astype(np.float32))
+    ctx = d.Context.default()
+    c0 = ctx.launch_count
+    d.gemm(A, B)
+    assert ctx.launch_count - c0 >= 3
