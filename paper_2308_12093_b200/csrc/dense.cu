@@ -3,7 +3,8 @@
 // column sums, and counter-based generation of the reference's random inputs.
 //
 // float32 X.Theta-class GEMMs go to the tcgen05 kernel in gemm_tc.cu when the
-// shape qualifies; this SIMT kernel handles float64 and odd shapes.
+// shape qualifies; float64 GEMMs run on the FP64 tensor cores (DMMA,
+// k_gemm_dmma); the SIMT kernel handles small float32 shapes.
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -99,6 +100,107 @@ __global__ void __launch_bounds__(256) k_gemm_simt(const T* __restrict__ A, cons
     }
 }
 
+// ---------------------------------------------------------------------------
+// float64 GEMM on the FP64 tensor cores: the same 64 x 64 x 16 shared-memory
+// tiles as k_gemm_simt, products by mma.sync.m8n8k4.f64 (DMMA).  8 warps as
+// 2 (M) x 4 (N), each warp a 32 x 16 sub-tile = 4 x 2 DMMA 8x8 accumulators.
+// Fragments (row.col): A 8x4 -- lane holds A[lane/4][lane%4]; B 4x8 -- lane
+// holds B[lane%4][lane/4]; C 8x8 -- lane holds C[lane/4][2(lane%4) + {0,1}].
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
+                                                   const double* __restrict__ B, int M, int N,
+                                                   int K, int lda, int ldb, bool ta, bool tb,
+                                                   int kchunk, double* __restrict__ part,
+                                                   double* __restrict__ C,
+                                                   const double* __restrict__ bias) {
+  __shared__ double As[GBK][GBM + 1];
+  __shared__ double Bs[GBK][GBN + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;  // warp sub-tile origin
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  const int k_begin = blockIdx.z * kchunk;
+  const int k_end = min(K, k_begin + kchunk);
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int k0 = k_begin; k0 < k_end; k0 += GBK) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int idx = tid + t * 256;
+      int mm, kk;
+      if (ta) {
+        mm = idx % GBM;
+        kk = idx / GBM;
+      } else {
+        kk = idx % GBK;
+        mm = idx / GBK;
+      }
+      const int gm = m0 + mm, gk = k0 + kk;
+      double v = 0.0;
+      if (gm < M && gk < k_end) v = ta ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int idx = tid + t * 256;
+      int nn, kk;
+      if (tb) {
+        kk = idx % GBK;
+        nn = idx / GBK;
+      } else {
+        nn = idx % GBN;
+        kk = idx / GBN;
+      }
+      const int gn = n0 + nn, gk = k0 + kk;
+      double v = 0.0;
+      if (gn < N && gk < k_end) v = tb ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < GBK; ks += 4) {
+      const int kr = ks + (lane & 3);
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kr][wm + 8 * i + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[kr][wn + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gm = m0 + wm + 8 * i + (lane >> 2);
+        const int gn = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (gm < M && gn < N) {
+          if (part) {
+            part[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j][h];
+          } else {
+            double v = acc[i][j][h];
+            if (bias) v = add_rn(v, bias[gn]);
+            C[(int64_t)gm * N + gn] = v;
+          }
+        }
+      }
+}
+
 template <class T, class Acc>
 __global__ void k_splitk_reduce(int splits, int64_t MN, int N, const Acc* __restrict__ part,
                                 T* __restrict__ C, const T* __restrict__ bias) {
@@ -128,7 +230,17 @@ void gemm_simt(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int
   if (K == 0) kchunk = GBK;
   splits = K == 0 ? 1 : (int)ceil_div(K, kchunk);
   dim3 grid((unsigned)ceil_div(N, GBN), (unsigned)ceil_div(M, GBM), (unsigned)splits);
+  // float64 on the FP64 tensor cores (DMMA) unless disabled (dev switch)
+  static const bool simt64 = getenv("SGNN_DMMA_OFF") != nullptr;
+  const bool dmma = sizeof(T) == 8 && !simt64;
   if (splits == 1) {
+    if constexpr (sizeof(T) == 8)
+      if (dmma) {
+        k_gemm_dmma<<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
+                                                   nullptr, C, bias);
+        launched(ctx);
+        return;
+      }
     k_gemm_simt<T, T><<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
                                                      (T*)nullptr, C, bias);
     launched(ctx);
@@ -136,8 +248,16 @@ void gemm_simt(sgnn_ctx ctx, const T* A, int32_t ra, int32_t ca, const T* B, int
     // float32 partials of <= kchunk terms, combined in float64 in slice order
     using Acc = T;
     DevBuf part((size_t)splits * M * N * sizeof(Acc), ctx->stream);
-    k_gemm_simt<T, Acc><<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
-                                                       part.as<Acc>(), C, bias);
+    bool done = false;
+    if constexpr (sizeof(T) == 8)
+      if (dmma) {
+        k_gemm_dmma<<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
+                                                   part.as<double>(), C, bias);
+        done = true;
+      }
+    if (!done)
+      k_gemm_simt<T, Acc><<<grid, 256, 0, ctx->stream>>>(A, B, M, N, K, ca, cb, ta, tb, kchunk,
+                                                         part.as<Acc>(), C, bias);
     launched(ctx);
     const int64_t MN = (int64_t)M * N;
     k_splitk_reduce<T, Acc><<<grid_for(ctx, MN, 256), 256, 0, ctx->stream>>>(
