@@ -104,9 +104,11 @@ def test_config2_arxiv_sweep(d, ref, orc, k, fg):
     check_all(orc, zip(("out", "d_theta", "d_bias", "d_input"), got, want))
 
 
-@pytest.mark.parametrize("policy", ["transform-first", "propagate-first"])
-def test_config2_forced_schemes(d, ref, orc, policy):
-    s, got, want = gcn_case(d, ref, 128, 64, True, policy=policy, caching=False)
+@pytest.mark.parametrize("policy,caching", [("transform-first", False), ("propagate-first", False),
+                                            ("propagate-first", True)])
+@pytest.mark.parametrize("k", [8, 64])
+def test_config2_forced_schemes(d, ref, orc, policy, caching, k):
+    s, got, want = gcn_case(d, ref, 128, k, True, policy=policy, caching=caching)
     check_all(orc, zip(("out", "d_theta", "d_bias", "d_input"), got, want))
 
 

@@ -156,10 +156,14 @@ def test_edge_softmax_requires_self_loops(d):
 # (5000, 96, 300): 160-wide tiles with a ragged last tile; stored widths that
 # are not multiples of 4 (Cora's 1433 features) run on tcgen05 from padded
 # staging copies: (2708, 1433, 16) pads K, (3000, 64, 1433) pads N (and K
-# with tb), (1433, 2708, 16) with ta pads M (the dTheta shape)
+# with tb), (1433, 2708, 16) with ta pads M (the dTheta shape); one tiny
+# dimension (skinny.cu): (20000, 128, 8) narrow N, (128, 20000, 8) with ta the
+# narrow dTheta, (20000, 8, 128) thin K, (8000, 1433, 16) Cora-wide K
 @pytest.mark.parametrize("shape", [(1000, 7, 5), (300, 128, 256), (4096, 64, 40), (70000, 16, 8),
                                    (20000, 256, 320), (5000, 96, 300), (2708, 1433, 16),
-                                   (3000, 64, 1433), (1433, 2708, 16)])
+                                   (3000, 64, 1433), (1433, 2708, 16), (20000, 128, 8),
+                                   (128, 20000, 8), (20000, 8, 128), (8000, 1433, 16),
+                                   (16, 9000, 4)])
 @pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True)])
 def test_gemm_vs_oracle(d, orc, shape, trans):
     n, m, k = shape
