@@ -65,6 +65,10 @@ struct sgnn_ctx_s {
   int num_sms = 148;
   int64_t launches = 0;
   sgnn::Pipe* pipe = nullptr;  // lazily created copy streams + staging buffers
+  // side stream for independent work inside one layer call (fork / join by
+  // events; captured into CUDA graphs with the main stream)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
 
 namespace sgnn {
@@ -93,6 +97,30 @@ class MemTrack {
   void on_reclass(int from, int to, size_t b);
   void stats(int c, int64_t* live, int64_t* peak, int64_t* total);  // c == 4: all classes
   void reset_peaks();
+};
+
+// Independent work inside one layer call on the context's side stream.  The
+// constructor forks (the side stream waits for the main stream's work so
+// far); side() / main() switch ctx->stream, so launches and stream-ordered
+// allocations go to that stream (the context is single-writer, so the swap is
+// safe); join() -- also run by the destructor -- makes the main stream wait
+// for the side stream.  Fork and join are events, so a captured step keeps
+// the concurrency in its CUDA graph.  SGNN_NO_FORK=1 keeps everything on the
+// main stream (same kernels, issue order).
+class SideStream {
+ public:
+  explicit SideStream(sgnn_ctx ctx);
+  ~SideStream() { join(); }
+  void side() {
+    if (active_) ctx_->stream = ctx_->aux;
+  }
+  void main() { ctx_->stream = main_; }
+  void join();
+
+ private:
+  sgnn_ctx ctx_;
+  cudaStream_t main_ = nullptr;
+  bool active_ = false;
 };
 
 // Stream-ordered device buffer (cudaMallocAsync from the pooled default mem

@@ -96,9 +96,17 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf S((size_t)n * k * sizeof(T), st);
       S.track(kTransient, S.bytes());  // gcn.hpp:152-155
+      const LongRows* bp = bwd_plan(ctx, A);
+      SideStream side(ctx);  // d_bias on the side stream, during the SpMM
+      side.side();
       column_sums<T>(ctx, G, n, k, d_bias);
-      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bwd_plan(ctx, A));
+      side.main();
+      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bp);
+      side.join();
+      SideStream side2(ctx);  // dTheta = X^T S on the side stream, dX = S Theta^T here
+      if (fg) side2.side();
       gemm<T>(ctx, X, n, m, S.as<T>(), n, k, true, false, d_theta);
+      side2.main();
       if (fg) {
         bool fused = false;
         if constexpr (sizeof(T) == 4)
@@ -115,29 +123,42 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       const T* X = static_cast<const T*>(c->saved_input);
       DevBuf P((size_t)n * m * sizeof(T), st);
       P.track(kTransient, P.bytes());  // gcn.hpp:163-167
-      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
+      const LongRows* fp = fwd_plan(ctx, A);
+      const LongRows* bp = fg ? bwd_plan(ctx, A) : nullptr;
+      // P = A'X -> dTheta (+ d_bias) on the side stream, G Theta^T -> A'^T G2
+      // on the main stream: independent chains, overlapped
+      SideStream side(ctx);
+      if (fg) side.side();
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fp);
       gemm_tn_colsum<T>(ctx, P.as<T>(), n, m, G, n, k, d_theta, d_bias);
+      side.main();
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         G2.track(kTransient, G2.bytes());
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
-                    bwd_plan(ctx, A));
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp);
         relu_bwd();
       }
+      side.join();
       break;
     }
     case SGNN_SPLIT_PROPAGATE_CACHED: {
       const T* P = c->saved_propagated.as<T>();
+      const LongRows* bp = fg ? bwd_plan(ctx, A) : nullptr;
+      // dTheta (+ d_bias) = P^T G on the side stream, overlapped with
+      // G Theta^T -> A'^T G2 on the main stream
+      SideStream side(ctx);
+      if (fg) side.side();
       gemm_tn_colsum<T>(ctx, P, n, m, G, n, k, d_theta, d_bias);
+      side.main();
       if (fg) {
-        DevBuf G2((size_t)n * m * sizeof(T), st);
+        DevBuf G2((size_t)n * m * sizeof(T), ctx->stream);
         G2.track(kTransient, G2.bytes());  // gcn.hpp:180-184
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz,
-                    bwd_plan(ctx, A));
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp);
         relu_bwd();
       }
+      side.join();
       break;
     }
     default: throw invalid_argument("gcn_backward: unknown scheme");

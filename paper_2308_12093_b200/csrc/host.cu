@@ -62,6 +62,27 @@ void MemTrack::reset_peaks() {  // peaks restart from the live level (memtrack.h
     k->total = 0;
   }
 }
+
+SideStream::SideStream(sgnn_ctx ctx) : ctx_(ctx), main_(ctx->stream) {
+  static const bool off = getenv("SGNN_NO_FORK") != nullptr;
+  if (off) return;
+  if (!ctx->aux) {
+    SGNN_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    SGNN_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    SGNN_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  }
+  SGNN_CUDA(cudaEventRecord(ctx->fork_ev, main_));
+  SGNN_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
+  active_ = true;
+}
+
+void SideStream::join() {
+  ctx_->stream = main_;
+  if (!active_) return;
+  active_ = false;
+  cudaEventRecord(ctx_->join_ev, ctx_->aux);
+  cudaStreamWaitEvent(main_, ctx_->join_ev, 0);
+}
 }  // namespace sgnn
 
 using namespace sgnn;
@@ -107,6 +128,12 @@ int sgnn_ctx_create(int device, void* stream, sgnn_ctx* out) {
 int sgnn_ctx_destroy(sgnn_ctx ctx) {
   SGNN_API_BEGIN
   if (!ctx) return SGNN_OK;
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+    cudaEventDestroy(ctx->fork_ev);
+    cudaEventDestroy(ctx->join_ev);
+  }
   if (ctx->pipe) {
     cudaStreamSynchronize(ctx->stream);
     destroy_pipe(ctx);
