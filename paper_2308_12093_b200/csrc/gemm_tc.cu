@@ -1062,6 +1062,14 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
       sp = (int)std::min<int64_t>(ctx->num_sms / tl, ksteps / 8);
       if (sp < 1) sp = 1;
     }
+    // accuracy: a split sums its k-block results in float32 registers (drain
+    // mode), so its rounding error grows with its k-block count.  Above
+    // kMaxDrainBlocks per split (K > ~4k rows per split: config 5's dTheta
+    // over n = 2.45M rows) use more splits -- several waves -- so the float32
+    // part stays as short as at Arxiv and the splits combine in float64.
+    constexpr int kMaxDrainBlocks = 128;
+    if (drain && ksteps > (int64_t)kMaxDrainBlocks * sp)
+      sp = (int)ceil_div(ksteps, kMaxDrainBlocks);
     return sp;
   };
   // Small B (the parameter matrix Theta): split hi/lo once in global memory so

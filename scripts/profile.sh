@@ -7,7 +7,7 @@ set -x
 TAG=${1:-r1}
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches_${TAG}.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-model-cpu > gpurun_out/launches_${TAG}.log 2>&1
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-model-cpu --no-large --no-parity > gpurun_out/launches_${TAG}.log 2>&1
 ONE=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"k_|gemm|split" --csv --log-file gpurun_out/gat_launches_${TAG}.csv \
     python scripts/kbench.py gat > gpurun_out/gat_launches_${TAG}.log 2>&1
@@ -16,7 +16,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     python scripts/dev/gat2_step.py 256 > gpurun_out/gat2_launches_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_spmm_lean|k_gemm_tc|k_colsum" \
     -s 12 -c 6 -o gpurun_out/full_${TAG} \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-model-cpu > gpurun_out/full_${TAG}.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-model-cpu --no-large --no-parity > gpurun_out/full_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on \
     -k regex:"k_gat_attn4|k_gat_agg2|k_gat_sddmm2|k_gat_sbwd4|k_gat_col2|k_node_scores" \
     -s 6 -c 6 -o gpurun_out/full_gat_${TAG} \

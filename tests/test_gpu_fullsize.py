@@ -206,3 +206,44 @@ def test_config4_model_step(d, ref, orc, kind, hid):
     print(f"\n{kind} hid={hid}: gradient error / max|gradient| = "
           f"{np.abs(gg - gw).max() / np.abs(gw).max():.3e}")
     assert abs(float(loss) - want[0]) <= TOL * max(1.0, abs(want[0]))
+
+
+# ---- config 5 at one GPU: the large power-law graph ----------------------------
+LARGE = (2449029, 61859140 / 2449029)
+
+
+def test_config5_powerlaw_gcn_layer(d, ref, orc):
+    """A config-5 GCN layer (100 -> 256, fg, adaptive + caching) on the
+    2.45M-node / 64M-edge power-law graph (maximum degree ~1e5: the hub-row
+    segment plans) against the reference in float64 on the same COO."""
+    n, m, k = LARGE[0], 100, 256
+    src, dst = d.powerlaw_graph(n, LARGE[1], 2.5, SEED)
+    A = d.Adjacency.gcn_operator(n, src, dst, torch.float32, "csc")
+    X = d.random_uniform(n, m, SEED + 11)
+    G = d.random_uniform(n, k, SEED + 12)
+    theta, bias = d.gcn_params(m, k, SEED + 13)
+    s = d.resolve_scheme("adaptive", m, k, True, True)
+    out, cache = d.gcn_forward(A, X, theta, bias, s)
+    got = (out,) + d.gcn_backward(A, G, theta, cache, True)
+    coo = ref.gcn_normalize(n, src.cpu().numpy(), dst.cpu().numpy())
+    assert coo[0].size == A.nnz
+    want = ref.gcn_layer(n, coo, 2, h64(X), h64(theta), h64(bias),
+                         (s.forward, s.backward, s.caching), h64(G), True)
+    check_all(orc, zip(("out", "d_theta", "d_bias", "d_input"), got, want))
+
+
+def test_config5_powerlaw_gat_forward(d, ref, orc):
+    """The config-5 GAT layer's forward (100 -> 8 x 32) on the power-law
+    pattern against the reference in float64 (the output is continuous in
+    the scores; the LeakyReLU-decision caveat above concerns gradients)."""
+    n, m, h, k = LARGE[0], 100, 8, 32
+    src, dst = d.powerlaw_graph(n, LARGE[1], 2.5, SEED)
+    P = d.Pattern.gat_pattern(n, src, dst)
+    X = d.random_uniform(n, m, SEED + 11)
+    th, a_s, a_d, b = d.gat_params(m, h, k, SEED + 13)
+    out, _ = d.gat_forward(P, X, th, a_s, a_d, b, h, 0.2, "none")
+    pa = P.arrays()
+    rp, cl = pa["rowptr"].cpu().numpy(), pa["cols"].cpu().numpy()
+    G0 = np.zeros((n, h * k))
+    want = ref.gat_layer(n, rp, cl, *[h64(x) for x in (X, th, a_s, a_d, b)], h, 0, G0, False)[0]
+    check_all(orc, [("out", out, want)])
