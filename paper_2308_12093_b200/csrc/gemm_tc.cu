@@ -950,11 +950,18 @@ static bool tc_disabled() {
 // with zero columns (and zero K rows) -- the extra products are exact zeros.
 __global__ void k_pad2d(int32_t rows, int32_t cols, const float* __restrict__ src, int32_t ld,
                         int32_t orows, int32_t ocols, float* __restrict__ dst) {
-  const int64_t total = (int64_t)orows * ocols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = (int32_t)(i / ocols), c = (int32_t)(i % ocols);
-    dst[i] = (r < rows && c < cols) ? __ldg(src + (int64_t)r * ld + c) : 0.f;
+  // a warp per output row (grid-stride), lanes over columns: coalesced
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < orows;
+       r += nw) {
+    const float* s = src + r * ld;
+    float* d = dst + r * ocols;
+    if (r < rows) {
+      for (int32_t c = lane; c < ocols; c += 32) d[c] = c < cols ? __ldg(s + c) : 0.f;
+    } else {
+      for (int32_t c = lane; c < ocols; c += 32) d[c] = 0.f;
+    }
   }
 }
 
@@ -1034,9 +1041,12 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
   if (M <= 0 || N <= 0 || K <= 0) return false;
   if ((int64_t)M * N * K < (int64_t)1 << 20) return false;  // tiny: SIMT is fine
-  if ((ca & 3) || (cb & 3))  // 16-byte row pitches for TMA: stage padded operands
+  static const bool no_pad = getenv("SGNN_NO_PAD") != nullptr;  // dev switch
+  if ((ca & 3) || (cb & 3)) {  // 16-byte row pitches for TMA: stage padded operands
+    if (no_pad) return false;
     return gemm_tc_f32_padded(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, colsum_b, att_src,
                               att_dst, s_out, d_out, heads, relu_out, mask_in, elu_saved);
+  }
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
   if ((reinterpret_cast<uintptr_t>(C) & 15) || (bias && (reinterpret_cast<uintptr_t>(bias) & 15)))
     return false;
@@ -1067,7 +1077,10 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     // kMaxDrainBlocks per split (K > ~4k rows per split: config 5's dTheta
     // over n = 2.45M rows) use more splits -- several waves -- so the float32
     // part stays as short as at Arxiv and the splits combine in float64.
-    constexpr int kMaxDrainBlocks = 128;
+    static const int kMaxDrainBlocks = [] {  // dev knob SGNN_DRAIN_MAX (default 128)
+      const char* e = getenv("SGNN_DRAIN_MAX");
+      return e ? atoi(e) : 128;
+    }();
     if (drain && ksteps > (int64_t)kMaxDrainBlocks * sp)
       sp = (int)ceil_div(ksteps, kMaxDrainBlocks);
     return sp;
