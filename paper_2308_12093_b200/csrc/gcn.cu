@@ -48,13 +48,15 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
     DevBuf M((size_t)n * k * sizeof(T), st);
     M.track(kTransient, M.bytes());  // gcn.hpp:103-106
     gemm<T>(ctx, X, n, m, theta, m, k, false, false, M.as<T>());
-    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz, fwd_plan(ctx, A));
+    spmm_csr<T>(ctx, n, rp, ci, av, M.as<T>(), k, out, bias, A->nnz, fwd_plan(ctx, A),
+                A->n_cols);
     if (relu) ok(sgnn_activation(ctx, 0, dt<T>(), out, (int64_t)n * k, out, relu));
     c->saved_input = X;
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
     P.track(kTransient, P.bytes());  // gcn.hpp:114-117
-    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A));
+    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A),
+                A->n_cols);
     bool fused = false;
     if constexpr (sizeof(T) == 4)
       if (relu) fused = gemm_relu_f32(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias,
@@ -101,7 +103,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       side.side();
       column_sums<T>(ctx, G, n, k, d_bias);
       side.main();
-      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bp);
+      spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G, k, S.as<T>(), nullptr, A->nnz, bp, n);
       side.join();
       SideStream side2(ctx);  // dTheta = X^T S on the side stream, dX = S Theta^T here
       if (fg) side2.side();
@@ -129,14 +131,14 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
       // on the main stream: independent chains, overlapped
       SideStream side(ctx);
       if (fg) side.side();
-      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fp);
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fp, A->n_cols);
       gemm_tn_colsum<T>(ctx, P.as<T>(), n, m, G, n, k, d_theta, d_bias);
       side.main();
       if (fg) {
         DevBuf G2((size_t)n * m * sizeof(T), st);
         G2.track(kTransient, G2.bytes());
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp, n);
         relu_bwd();
       }
       side.join();
@@ -155,7 +157,7 @@ void gcn_backward_t(sgnn_ctx ctx, sgnn_adj A, const T* G, const T* theta, int32_
         DevBuf G2((size_t)n * m * sizeof(T), ctx->stream);
         G2.track(kTransient, G2.bytes());  // gcn.hpp:180-184
         gemm<T>(ctx, G, n, k, theta, m, k, false, true, G2.as<T>());
-        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp);
+        spmm_csr<T>(ctx, A->n_cols, cp, cr, cv, G2.as<T>(), m, d_input, nullptr, A->nnz, bp, n);
         relu_bwd();
       }
       side.join();

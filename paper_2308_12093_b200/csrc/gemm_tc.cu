@@ -967,6 +967,33 @@ __global__ void k_pad2d(int32_t rows, int32_t cols, const float* __restrict__ sr
 
 static int32_t round4(int32_t x) { return (x + 3) & ~3; }
 
+// dst (rows x ocols) = src (rows x cols, pitch ld) + bias, dropping padding
+__global__ void k_unpad2d(int32_t rows, int32_t ocols, const float* __restrict__ src, int32_t ld,
+                          const float* __restrict__ bias, float* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += nw)
+    for (int32_t c = lane; c < ocols; c += 32) {
+      const float v = __ldg(src + r * ld + c);
+      dst[r * ocols + c] = bias ? v + __ldg(bias + c) : v;
+    }
+}
+
+void pad_rows_f32(sgnn_ctx ctx, int32_t rows, int32_t cols, const float* src, int32_t ld,
+                  int32_t ocols, float* dst) {
+  k_pad2d<<<grid_for(ctx, (int64_t)rows * 32, 256), 256, 0, ctx->stream>>>(rows, cols, src, ld,
+                                                                            rows, ocols, dst);
+  launched(ctx);
+}
+
+void unpad_rows_f32(sgnn_ctx ctx, int32_t rows, int32_t ocols, const float* src, int32_t ld,
+                    const float* bias, float* dst) {
+  k_unpad2d<<<grid_for(ctx, (int64_t)rows * 32, 256), 256, 0, ctx->stream>>>(rows, ocols, src, ld,
+                                                                              bias, dst);
+  launched(ctx);
+}
+
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src, const float* att_dst, float* s_out,

@@ -127,11 +127,20 @@ int gcn_backward_relu(sgnn_ctx ctx, sgnn_adj A, const void* d_out, const void* t
                       int32_t k, sgnn_gcn_cache c, int fg, void* d_theta, void* d_bias,
                       void* d_input, const uint8_t* relu_mask_in);
 
-// C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals)
+// C (n_rows x f) = A B (+bias) for a CSR (rowptr, cols, vals); b_rows = the
+// row count of B when known (float32 widths that are not a multiple of 4 are
+// then staged into 16-byte-aligned padded copies for the vector kernels)
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
               const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz,
-              const LongRows* lr = nullptr);
+              const LongRows* lr = nullptr, int32_t b_rows = -1);
+
+// row-padded staging copies of float32 matrices (gemm_tc.cu): zero-padded to
+// ocols columns / back to ocols columns with an optional bias add
+void pad_rows_f32(sgnn_ctx ctx, int32_t rows, int32_t cols, const float* src, int32_t ld,
+                  int32_t ocols, float* dst);
+void unpad_rows_f32(sgnn_ctx ctx, int32_t rows, int32_t ocols, const float* src, int32_t ld,
+                    const float* bias, float* dst);
 
 // C = op(A) op(B) (row-major); A ra x ca, B rb x cb; bias added per column of C
 template <class T>

@@ -555,9 +555,26 @@ static void launch_w(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const 
 template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
               const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz,
-              const LongRows* lr) {
+              const LongRows* lr, int32_t b_rows) {
   if (n_rows == 0 || f == 0) return;
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  if constexpr (sizeof(T) == 4) {
+    // widths that are not a multiple of 4 (config 5's 47 classes): the scalar
+    // kernel gathers 188-byte rows 4 bytes per lane; staging B into a
+    // 16-byte-aligned padded copy lets the float4 kernels run (the padding
+    // columns are zeros and never reach C; per-element order unchanged, so
+    // the result is bit-identical).  Only for large products with known B.
+    static const bool no_pad = getenv("SGNN_NO_PAD") != nullptr;
+    if (!no_pad && b_rows > 0 && f % 4 != 0 && f > 4 && nnz >= (int64_t)1 << 20) {
+      const int32_t f4 = (f + 3) & ~3;
+      DevBuf bp((size_t)b_rows * f4 * 4, ctx->stream), cp((size_t)n_rows * f4 * 4, ctx->stream);
+      pad_rows_f32(ctx, b_rows, f, B, f, f4, bp.as<float>());
+      spmm_csr<float>(ctx, n_rows, rowptr, cols, vals, bp.as<float>(), f4, cp.as<float>(),
+                      nullptr, nnz, lr, -1);
+      unpad_rows_f32(ctx, n_rows, f, cp.as<float>(), f4, bias, C);
+      return;
+    }
+  }
   const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(C) % 16 == 0) &&
                        (!bias || reinterpret_cast<uintptr_t>(bias) % 16 == 0);
@@ -590,10 +607,10 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
 
 template void spmm_csr<float>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const float*,
                               const float*, int32_t, float*, const float*, int64_t,
-                              const LongRows*);
+                              const LongRows*, int32_t);
 template void spmm_csr<double>(sgnn_ctx, int32_t, const int32_t*, const int32_t*, const double*,
                                const double*, int32_t, double*, const double*, int64_t,
-                               const LongRows*);
+                               const LongRows*, int32_t);
 
 }  // namespace sgnn
 
@@ -611,7 +628,8 @@ extern "C" int sgnn_spmm(sgnn_ctx ctx, sgnn_adj adj, int transposed, const void*
   if (adj->dtype == SGNN_F32) {
     const float* v = transposed ? adj->cvals.as<float>() : adj->vals.as<float>();
     spmm_csr<float>(ctx, n_out, ptr, idx, v, static_cast<const float*>(B), f,
-                    static_cast<float*>(C), static_cast<const float*>(bias), adj->nnz, lr);
+                    static_cast<float*>(C), static_cast<const float*>(bias), adj->nnz, lr,
+                    transposed ? adj->n_rows : adj->n_cols);
   } else {
     const double* v = transposed ? adj->cvals.as<double>() : adj->vals.as<double>();
     spmm_csr<double>(ctx, n_out, ptr, idx, v, static_cast<const double*>(B), f,
