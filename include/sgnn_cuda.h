@@ -233,6 +233,14 @@ int sgnn_gemm(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, co
 int sgnn_gemm_ex(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
                  int32_t rb, int32_t cb, int trans_a, int trans_b, void* C, const void* bias,
                  void* colsum_b);
+/* gemm + activation (dense.hpp:197-268), the activation fused into the
+ * tcgen05 epilogue where the shape allows it, else two passes (identical
+ * results): act 0 = ReLU forward (C = relu(op(A) op(B) + bias), mask out),
+ * 1 = ReLU backward (C zeroed where mask == 0), 2 = ELU(1) backward (C times
+ * saved + 1 where mask == 0; saved = the ELU output); bias only with act 0 */
+int sgnn_gemm_act(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+                  int32_t rb, int32_t cb, int ta, int tb, void* C, const void* bias, int act,
+                  uint8_t* mask, const void* saved);
 /* dense.hpp:272-282 column_sums: out (cols) = sum over rows */
 int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
                      void* out);

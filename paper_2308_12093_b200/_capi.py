@@ -107,6 +107,7 @@ _SIGS = {
     "sgnn_gcn_step_host": (INT, [VP, VP, VP, I32, VP, VP, I32, C.POINTER(Scheme), VP, INT, VP, VP,
                                  VP, VP]),
     "sgnn_mem_stats": (INT, [INT, PI64, PI64, PI64]),
+    "sgnn_gemm_act": (INT, [VP, INT, VP, I32, I32, VP, I32, I32, INT, INT, VP, VP, INT, VP, VP]),
     "sgnn_gcn_cache_arrays": (INT, [VP, PVP, PVP]),
     "sgnn_gat_cache_arrays": (INT, [VP, PVP, PVP, PVP, PVP, PVP]),
     "sgnn_mem_reset_peaks": (INT, []),

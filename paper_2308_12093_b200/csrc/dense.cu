@@ -575,6 +575,48 @@ int sgnn_gemm_ex(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca,
   SGNN_API_END
 }
 
+static void ok_rc(int rc) {
+  if (rc == SGNN_OK) return;
+  if (rc == SGNN_EINVAL) throw invalid_argument(sgnn_last_error());
+  throw std::runtime_error(sgnn_last_error());
+}
+
+// gemm + activation (dense.hpp:197-268) with the activation fused into the
+// tcgen05 epilogue where the shape allows it (float32), else two passes with
+// identical results: act 0 = ReLU forward (C = relu(op(A) op(B) + bias),
+// mask out), 1 = ReLU backward (C zeroed where mask == 0), 2 = ELU(1)
+// backward (C scaled by saved + 1 where mask == 0; saved = the ELU output)
+int sgnn_gemm_act(sgnn_ctx ctx, int dtype, const void* A, int32_t ra, int32_t ca, const void* B,
+                  int32_t rb, int32_t cb, int ta, int tb, void* C, const void* bias, int act,
+                  uint8_t* mask, const void* saved) {
+  SGNN_API_BEGIN
+  require(act >= 0 && act <= 2 && mask != nullptr, "gemm_act: unknown activation");
+  require(act != 2 || saved != nullptr, "activation_backward: elu needs the saved output");
+  const int64_t count = (int64_t)(ta ? ca : ra) * (tb ? rb : cb);
+  bool fused = false;
+  if (dtype == SGNN_F32 && !getenv("SGNN_NO_ACT_FUSION")) {
+    const float* a = static_cast<const float*>(A);
+    const float* b = static_cast<const float*>(B);
+    float* c = static_cast<float*>(C);
+    if (act == 0)
+      fused = gemm_relu_f32(ctx, a, ra, ca, b, rb, cb, ta, tb, c,
+                            static_cast<const float*>(bias), mask, nullptr);
+    else if (act == 1 && !bias)
+      fused = gemm_relu_f32(ctx, a, ra, ca, b, rb, cb, ta, tb, c, nullptr, nullptr, mask);
+    else if (act == 2 && !bias)
+      fused = gemm_elu_bwd_f32(ctx, a, ra, ca, b, rb, cb, ta, tb, c, mask,
+                               static_cast<const float*>(saved));
+  }
+  if (!fused) {
+    DISPATCH_T(dtype, gemm<T>(ctx, static_cast<const T*>(A), ra, ca, static_cast<const T*>(B), rb,
+                              cb, ta != 0, tb != 0, static_cast<T*>(C),
+                              static_cast<const T*>(bias)));
+    if (act == 0) ok_rc(sgnn_activation(ctx, 0, dtype, C, count, C, mask));
+    else ok_rc(sgnn_activation_backward(ctx, act == 1 ? 0 : 2, dtype, C, mask, saved, count, C));
+  }
+  SGNN_API_END
+}
+
 int sgnn_column_sums(sgnn_ctx ctx, int dtype, const void* X, int32_t rows, int32_t cols,
                      void* out) {
   SGNN_API_BEGIN

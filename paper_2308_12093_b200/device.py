@@ -396,6 +396,27 @@ def gemm(A, B, trans_a=False, trans_b=False, ctx=None, bias=None, out=None, cols
     return out
 
 
+_GEMM_ACT = {"relu": 0, "relu_backward": 1, "elu_backward": 2}
+
+
+def gemm_act(A, B, act, mask, trans_a=False, trans_b=False, bias=None, saved=None, out=None,
+             ctx=None):
+    """C = op(A) op(B) (+ bias) followed by an activation, fused into the
+    tcgen05 epilogue where the shape allows it: act "relu" (writes `mask`),
+    "relu_backward" / "elu_backward" (reads `mask`, and `saved` = the ELU
+    output)."""
+    ctx = _ctx(ctx)
+    A, B = A.contiguous(), B.contiguous()
+    m = A.shape[1] if trans_a else A.shape[0]
+    n = B.shape[0] if trans_b else B.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=A.dtype, device=A.device)
+    check(lib.sgnn_gemm_act(ctx.handle, _dt(A), _p(A), A.shape[0], A.shape[1], _p(B), B.shape[0],
+                            B.shape[1], int(trans_a), int(trans_b), _p(out), _p(bias),
+                            _GEMM_ACT[act], _p(mask), _p(saved)))
+    return out
+
+
 def column_sums(X, ctx=None):
     ctx = _ctx(ctx)
     X = X.contiguous()

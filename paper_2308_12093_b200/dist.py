@@ -193,6 +193,13 @@ class DeviceOps:
     def colsum(self, X):
         return self.d.column_sums(X, ctx=self.ctx)
 
+    def gemm_act(self, A, B, act, mask, ta=False, tb=False, bias=None, saved=None):
+        """gemm + activation, fused into the tcgen05 epilogue where possible"""
+        return self.d.gemm_act(A, B, act, mask, ta, tb, bias=bias, saved=saved, ctx=self.ctx)
+
+    def mask(self, rows, cols):
+        return torch.empty((rows, cols), dtype=torch.uint8, device=self.dev)
+
     # model pieces (dense.hpp:196-270, model.hpp loss_mse)
     def activation(self, X, kind, out=None):
         return self.d.activation(X, kind, out=out, ctx=self.ctx)
@@ -229,9 +236,6 @@ class GatDeviceOps(DeviceOps):
 
     def stats_supported(self, h, k):
         return bool(self.c.lib.sgnn_gat_column_stats_supported(h, k))
-
-    def mask(self, rows, h):
-        return torch.empty((rows, h), dtype=torch.uint8, device=self.dev)
 
     @staticmethod
     def _p(t):
@@ -382,7 +386,10 @@ class DistGcnLayer:
         with _scope(self.ops):
             return self._forward(X_local, theta, bias, scheme, static_input)
 
-    def _forward(self, X_local, theta, bias, scheme, static_input):
+    def _forward(self, X_local, theta, bias, scheme, static_input, relu_mask=None):
+        """relu_mask (optional, uint8 like out): out = ReLU(layer) with its
+        mask (dense.hpp:197-228), fused into the output GEMM's epilogue for
+        the propagate-first schemes."""
         fwd = scheme[0]
         ops = self.ops
         cache = {"scheme": scheme}
@@ -390,11 +397,17 @@ class DistGcnLayer:
             buf, mine = self._buffer(theta.shape[1], X_local.dtype)
             ops.gemm(X_local, theta, out=mine)
             out = ops.spmm(self.A, self._exchange(buf), bias)
+            if relu_mask is not None:
+                out, m = ops.activation(out, "relu", out=out)
+                relu_mask.copy_(m)
             cache["X"] = X_local
         else:  # propagate-first: gather X, P_p = A'_p X, out = P_p Theta + b
             X = self.gather_static(X_local) if static_input else self.gather(X_local)
             P = ops.spmm(self.A, X)
-            out = ops.gemm(P, theta, bias=bias)
+            if relu_mask is not None:
+                out = ops.gemm_act(P, theta, "relu", relu_mask, bias=bias)
+            else:
+                out = ops.gemm(P, theta, bias=bias)
             if fwd == 2:
                 cache["P"] = P
             else:
@@ -406,7 +419,9 @@ class DistGcnLayer:
         with _scope(self.ops):
             return self._backward(G_local, theta, cache, needs_feature_grad)
 
-    def _backward(self, G_local, theta, cache, needs_feature_grad):
+    def _backward(self, G_local, theta, cache, needs_feature_grad, relu_mask=None):
+        """relu_mask (optional): d_input gets the ReLU backward of the layer
+        below applied (fused into the d_input GEMM for the fused scheme)."""
         ops = self.ops
         bwd = cache["scheme"][1]
         d_input = None
@@ -419,6 +434,9 @@ class DistGcnLayer:
             S = ops.spmm(self.AT, buf)
             d_theta, d_bias = self._allreduce(ops.gemm(cache["X"], S, ta=True), d_bias)
             if needs_feature_grad:
+                if relu_mask is not None:
+                    return d_theta, d_bias, ops.gemm_act(S, theta, "relu_backward", relu_mask,
+                                                         tb=True)
                 d_input = ops.gemm(S, theta, tb=True)
         else:
             w, buf = None, None
@@ -437,6 +455,8 @@ class DistGcnLayer:
             d_theta, d_bias = self._allreduce(d_theta, d_bias)
             if needs_feature_grad:
                 d_input = ops.spmm(self.AT, buf)
+        if relu_mask is not None and d_input is not None:
+            d_input = ops.activation_backward(d_input, relu_mask, "relu", out=d_input)
         return d_theta, d_bias, d_input
 
     def step_host(self, hX, theta, bias, scheme, hG, needs_feature_grad, h_out, h_d_theta,
@@ -519,14 +539,15 @@ class DistGcn2:
         with _scope(L.ops):
             ops = L.ops
             th1, b1, th2, b2 = self.p
-            h, c1 = L._forward(X_local, th1, b1, self.s1, static_input)
-            h, mask = ops.activation(h, "relu", out=h)
+            # ReLU fused into the layer-1 output GEMM and, backwards, into the
+            # layer-2 d_input GEMM where the schemes allow it (as model.cu)
+            mask = ops.mask(L.r1 - L.r0, th1.shape[1])
+            h, c1 = L._forward(X_local, th1, b1, self.s1, static_input, relu_mask=mask)
             o, c2 = L._forward(h, th2, b2, self.s2, False)
             loss, g = ops.loss_mse(o, target_local, L.n * self.out)
             if L.world > 1:
                 dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=L.group)
-            dth2, db2, dh = L._backward(g, th2, c2, True)
-            dh = ops.activation_backward(dh, mask, "relu", out=dh)
+            dth2, db2, dh = L._backward(g, th2, c2, True, relu_mask=mask)
             dth1, db1, dx = L._backward(dh, th1, c1, self.input_grad)
         return loss, o, [dth1, db1, dth2, db2], dx
 
@@ -680,7 +701,9 @@ class DistGatLayer:
         with _scope(self.ops):
             return self._backward(G_local, theta, a_src, a_dst, cache, needs_feature_grad)
 
-    def _backward(self, G_local, theta, a_src, a_dst, cache, needs_feature_grad):
+    def _backward(self, G_local, theta, a_src, a_dst, cache, needs_feature_grad, elu=None):
+        """elu (optional): (mask, saved) of an ELU(1) below the layer; d_input
+        gets its backward, fused into the d_input GEMM epilogue."""
         ops, x = self.ops, self.x
         h, k, nl = self.h, self.k, self.r1 - self.r0
         hk = h * k
@@ -719,7 +742,10 @@ class DistGatLayer:
         d_ad = flat[theta.numel() + 2 * hk:].view(h, k)
         ops.param_grads(nl, h, k, Gmine, cache["Mmine"], dS, dD, d_b, d_as, d_ad)
         ops.gemm(cache["X"], dM, True, False, out=d_theta)
-        d_x = ops.gemm(dM, theta, False, True) if needs_feature_grad else None
+        d_x = None
+        if needs_feature_grad:
+            d_x = ops.gemm(dM, theta, False, True) if elu is None else \
+                ops.gemm_act(dM, theta, "elu_backward", elu[0], tb=True, saved=elu[1])
         x.allreduce(flat)
         return d_theta, d_as, d_ad, d_b, d_x
 
@@ -753,7 +779,7 @@ class DistGat2:
             loss, g = ops.loss_mse(o, target_local, L2.n * self.heads * self.out)
             if L2.world > 1:
                 dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=L2.group)
-            g2 = L2._backward(g, th2, as2, ad2, c2, True)
-            dh = ops.activation_backward(g2[4], mask, "elu", saved=h)
-            g1 = L1._backward(dh, th1, as1, ad1, c1, self.input_grad)
+            # the ELU backward fused into the layer-2 d_input GEMM (as model.cu)
+            g2 = L2._backward(g, th2, as2, ad2, c2, True, elu=(mask, h))
+            g1 = L1._backward(g2[4], th1, as1, ad1, c1, self.input_grad)
         return loss, o, list(g1[:4]) + list(g2[:4]), g1[4]

@@ -78,6 +78,18 @@ class CpuOps:
             r = out
         return r
 
+    def mask(self, rows, cols):
+        return torch.empty((rows, cols), dtype=torch.uint8)
+
+    def gemm_act(self, A, B, act, mask, ta=False, tb=False, bias=None, saved=None):
+        r = self.gemm(A, B, ta, tb, bias=bias)
+        if act == "relu":
+            r, m = self.activation(r, "relu", out=r)
+            mask.copy_(m)
+            return r
+        return self.activation_backward(r, mask, "relu" if act == "relu_backward" else "elu",
+                                        saved=saved)
+
     def loss_mse(self, out, target, total):
         d = out.numpy() - target.numpy()
         return torch.tensor(float((d * d).sum()) / total, dtype=torch.float64), \
@@ -102,9 +114,6 @@ class GatCpuOps(CpuOps):
 
     def stats_supported(self, h, k):
         return True
-
-    def mask(self, rows, h):
-        return torch.empty((rows, h), dtype=torch.uint8)
 
     def transform(self, X, theta, h, k, a_src, a_dst, M, s, d):
         m = (X @ theta).numpy()
