@@ -1116,7 +1116,11 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
         for (int t = 0; t < H; ++t) w[t] = lrelu(si[t] + dj[t], beta);
       }
 #pragma unroll
-      for (int t = 0; t < H; ++t) sm[t] += expf(w[t] - mx[t]);
+      for (int t = 0; t < H; ++t) {
+        const float ex = expf(w[t] - mx[t]);
+        sm[t] += ex;
+        if (one) w[t] = ex;  // single-pass rows keep exp(w - max) for alpha
+      }
     }
   }
   group_allreduce<H>(sm, gl, OpSum());
@@ -1130,9 +1134,9 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
     if (off + gl < deg) {
       float a[H];
       uint32_t pos = pos1;
-      if (one) {  // scores still in registers: no second gather
+      if (one) {  // exp(w - max) still in registers: no second gather or exp
 #pragma unroll
-        for (int t = 0; t < H; ++t) a[t] = expf(w[t] - mx[t]) * sm[t];
+        for (int t = 0; t < H; ++t) a[t] = w[t] * sm[t];
       } else {
         float dj[H];
         pos = 0;
