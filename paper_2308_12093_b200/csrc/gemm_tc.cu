@@ -790,9 +790,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 __global__ void __launch_bounds__(256) k_reduce_splits(int splits, int64_t MN, int N,
                                                        const float* __restrict__ part,
                                                        float* __restrict__ C, int ldc,
-                                                       const float* __restrict__ bias) {
+                                                       const float* __restrict__ bias,
+                                                       int cs_parts = 0,
+                                                       const double* __restrict__ cs_part = nullptr,
+                                                       float* __restrict__ cs_out = nullptr) {
   __shared__ double sh[8][33];
   const int g = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t nbc = (MN + 31) / 32;
+  if (blockIdx.x >= nbc) {  // the fused column sums (d_bias) of the same GEMM
+    const int n = (int)((blockIdx.x - nbc) * 32 + l);
+    double s = 0.0;
+    if (n < N)
+      for (int p = g; p < cs_parts; p += 8) s += cs_part[(int64_t)p * N + n];
+    sh[g][l] = s;
+    __syncthreads();
+    if (g == 0 && n < N) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += sh[k][l];
+      cs_out[n] = (float)t;
+    }
+    return;
+  }
   const int64_t x = blockIdx.x * 32LL + l;
   double s = 0.0;
   if (x < MN) {
@@ -1197,11 +1216,12 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   }
   if (splits > 1) {
     const int64_t MN = (int64_t)M * N;
-    k_reduce_splits<<<(unsigned)ceil_div(MN, 32), 256, 0, ctx->stream>>>(splits, MN, N, pp, C, N,
-                                                                         bias);
+    // split-K partials -> C, and the fused column sums in the same launch
+    const unsigned ncs = colsum_b ? (unsigned)ceil_div(N, 32) : 0u;
+    k_reduce_splits<<<(unsigned)ceil_div(MN, 32) + ncs, 256, 0, ctx->stream>>>(
+        splits, MN, N, pp, C, N, bias, splits * 4, cs, colsum_b);
     launched(ctx);
-  }
-  if (colsum_b) {
+  } else if (colsum_b) {
     k_colsum_parts<<<(unsigned)N, 256, 0, ctx->stream>>>(splits * 4, N, cs, colsum_b);
     launched(ctx);
   }
