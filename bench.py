@@ -562,6 +562,26 @@ def run_ours(args):
 LARGE_N, LARGE_EDGES, LARGE_M = 2449029, 61859140, 100
 
 
+def _large_step_bytes(name, n, q, m):
+    """Compulsory bytes of one config-5 model step (scripts/sweep.py formulas):
+    Gcn2 m-256-47 (layer 1 propagate-first cached, no input gradient; layer 2
+    transform-first / fused with input gradient), Gat2 m-(8x32)-(8x8) level
+    full, plus the MSE pass."""
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    import stepbytes as sw  # noqa: E402
+
+    class S:  # scheme stand-in
+        def __init__(self, f, b):
+            self.forward, self.backward = f, b
+
+    if name == "gcn2":
+        by = sw.gcn_step_bytes(S(2, 2), n, q, m, 256, False)
+        by += sw.gcn_step_bytes(S(0, 0), n, q, 256, 47, True)
+        return int(by + 12 * n * 47)
+    by = sw.gat_step_bytes("full", n, q, m, 8, 32) + sw.gat_step_bytes("full", n, q, 256, 8, 8)
+    return int(by + 12 * n * 64)
+
+
 def large_graph_steps(args, ctx, world, steps):
     import torch
     import torch.distributed as dist
@@ -626,8 +646,14 @@ def large_graph_steps(args, ctx, world, steps):
         step_ms = float(t.item())
         nnz = nnz_gcn if name == "gcn2" else nnz_gat
         out.setdefault("step_ms_rank0", {})[name] = [round(x, 2) for x in ms]
+        by = _large_step_bytes(name, n, nnz, LARGE_M)
+        hbm = _peaks()[0]
         out[name] = {"ms": round(step_ms, 3), "edges_per_s": round(2 * nnz / (step_ms * 1e-3), 1),
-                     "edges_per_s_note": "2 layers x nnz per step / step time (whole job)"}
+                     "edges_per_s_note": "2 layers x nnz per step / step time (whole job)",
+                     "algorithmic_bytes": by,
+                     "frac_hbm": round(by / (step_ms * 1e-3) / 1e9 / (hbm * world), 3),
+                     "frac_note": "the step's compulsory kernel bytes (DESIGN §3 formulas, "
+                                  "scripts/sweep.py) / time / (N x measured HBM copy GB/s)"}
         del model, tgt, Xl
     out["gcn2"]["shape"] = f"{LARGE_M}-256-47 adaptive+caching, MSE"
     out["gat2"]["shape"] = (f"{LARGE_M}-(8x32)-(8x8) h=8, exchange "
