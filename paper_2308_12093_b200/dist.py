@@ -157,6 +157,20 @@ class _Exchange:
         return flat
 
 
+def _rank_world(group):
+    """(rank, world) of a process group; a group object may instead carry its
+    own (`rank_world()`: the single-GPU multi-rank simulation of the tests)."""
+    if hasattr(group, "rank_world"):
+        return group.rank_world()
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _exchange_for(group, rank, world):
+    if hasattr(group, "exchange"):  # simulated group: its own collectives
+        return group.exchange(rank, world)
+    return _Exchange(group, rank, world)
+
+
 # ---------------------------------------------------------------------------
 # compute backends
 # ---------------------------------------------------------------------------
@@ -313,8 +327,7 @@ class DistGcnLayer:
 
     def __init__(self, n, rows, cols, vals, ops, dtype=torch.float32, group=None):
         self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
+        self.rank, self.world = _rank_world(group)
         r_np = _np(rows).astype(np.int64) if not isinstance(rows, torch.Tensor) else None
         if r_np is not None:
             rowptr = np.zeros(n + 1, np.int64)
@@ -329,7 +342,7 @@ class DistGcnLayer:
         self.r0, self.r1 = self.bounds[self.rank], self.bounds[self.rank + 1]
         self.mx = max(self.bounds[p + 1] - self.bounds[p] for p in range(self.world))
         self.ops, self.dtype = ops, dtype
-        self.x = _Exchange(group, self.rank, self.world)
+        self.x = _exchange_for(group, self.rank, self.world)
         nl = self.r1 - self.r0
         wide = self.world * self.mx
         r, c, v = row_block(rows, cols, vals, self.r0, self.r1)
@@ -545,8 +558,7 @@ class DistGcn2:
             h, c1 = L._forward(X_local, th1, b1, self.s1, static_input, relu_mask=mask)
             o, c2 = L._forward(h, th2, b2, self.s2, False)
             loss, g = ops.loss_mse(o, target_local, L.n * self.out)
-            if L.world > 1:
-                dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=L.group)
+            L.x.allreduce(loss)
             dth2, db2, dh = L._backward(g, th2, c2, True, relu_mask=mask)
             dth1, db1, dx = L._backward(dh, th1, c1, self.input_grad)
         return loss, o, [dth1, db1, dth2, db2], dx
@@ -627,9 +639,8 @@ class DistGatLayer:
             ops = GatDeviceOps(ops)
         self.ops = ops
         self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        self.x = _Exchange(group, self.rank, self.world)
+        self.rank, self.world = _rank_world(group)
+        self.x = _exchange_for(group, self.rank, self.world)
         self.n, self.h, self.k = n, heads, k
         self.bounds = partition_rows(rowptr, self.world)
         self.r0, self.r1 = self.bounds[self.rank], self.bounds[self.rank + 1]
@@ -777,8 +788,7 @@ class DistGat2:
             h, mask = ops.activation(h, "elu", out=h)
             o, c2 = L2._forward(h, th2, as2, ad2, b2, self.beta)
             loss, g = ops.loss_mse(o, target_local, L2.n * self.heads * self.out)
-            if L2.world > 1:
-                dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=L2.group)
+            L2.x.allreduce(loss)
             # the ELU backward fused into the layer-2 d_input GEMM (as model.cu)
             g2 = L2._backward(g, th2, as2, ad2, c2, True, elu=(mask, h))
             g1 = L1._backward(g2[4], th1, as1, ad1, c1, self.input_grad)
