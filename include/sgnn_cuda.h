@@ -270,11 +270,27 @@ int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, con
                      const void* a_src, const void* a_dst, const void* bias, int32_t heads,
                      int32_t k, double beta, int level, int dtype, void* out,
                      sgnn_gat_cache* cache);
+/* gat_forward with options.  SGNN_GAT_REORDER lets the layer run operator-
+ * reordered when the heads are wider than the input (k > m; float32, h in
+ * {1,2,4,8}, m and k multiples of 4, no rows over 128 edges): the attention
+ * scores as X (Theta_t a_t), the aggregation over the m-wide input rows
+ * (Z_t = sum_j alpha_t X_j) and out_t = Z_t Theta_t + b_t, so M = X Theta is
+ * never formed -- same outputs and gradients within float32 rounding.  Such a
+ * cache keeps Z (n x h x m) where the reference keeps M (gat_cache_arrays
+ * returns M = NULL; extra_bytes counts Z); backward and edge_values accept it
+ * as any other.  Without the flag this is sgnn_gat_forward. */
+#define SGNN_GAT_REORDER 1
+int sgnn_gat_forward_ex(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
+                        const void* a_src, const void* a_dst, const void* bias, int32_t heads,
+                        int32_t k, double beta, int level, int dtype, void* out,
+                        sgnn_gat_cache* cache, int flags);
 int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
                       const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
                       double beta, sgnn_gat_cache cache, int needs_feature_grad, void* d_theta,
                       void* d_a_src, void* d_a_dst, void* d_bias, void* d_input);
 int sgnn_gat_cache_destroy(sgnn_gat_cache cache);
+/* 1 when the forward ran operator-reordered (sgnn_gat_forward_ex) */
+int sgnn_gat_cache_reordered(sgnn_gat_cache cache, int* out);
 /* gat.hpp:66-71 extra_bytes (== gat_cache_footprint at every level) */
 int sgnn_gat_cache_extra_bytes(sgnn_gat_cache cache, int64_t* out);
 /* gat.hpp:56-72 GatCache fields retained at the cache level (NULL otherwise):

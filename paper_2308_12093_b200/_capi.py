@@ -28,6 +28,7 @@ FWD_NAMES = ["transform_first", "propagate_first", "propagate_first_cached"]
 BWD_NAMES = ["fused_propagate", "split_propagate", "split_propagate_cached"]
 POLICIES = {"adaptive": 0, "transform-first": 1, "propagate-first": 2}
 LEVELS = {"none": 0, "features": 1, "node-attn": 2, "full": 3}
+GAT_REORDER = 1  # sgnn_gat_forward_ex flags (SGNN_GAT_REORDER)
 
 
 class ModelConfig(C.Structure):
@@ -110,6 +111,9 @@ _SIGS = {
     "sgnn_gemm_act": (INT, [VP, INT, VP, I32, I32, VP, I32, I32, INT, INT, VP, VP, INT, VP, VP]),
     "sgnn_gcn_cache_arrays": (INT, [VP, PVP, PVP]),
     "sgnn_gat_cache_arrays": (INT, [VP, PVP, PVP, PVP, PVP, PVP]),
+    "sgnn_gat_cache_reordered": (INT, [VP, C.POINTER(C.c_int)]),
+    "sgnn_gat_forward_ex": (INT, [VP, VP, VP, I32, VP, VP, VP, VP, I32, I32, D, INT, INT, VP, PVP,
+                                  INT]),
     "sgnn_mem_reset_peaks": (INT, []),
     "sgnn_gat_transform": (INT, [VP, VP, I32, I32, VP, I32, I32, VP, VP, VP, VP, VP]),
     "sgnn_rowplan_create": (INT, [VP, I32, VP, PVP]),

@@ -77,6 +77,7 @@ __device__ __forceinline__ void vstore(T* p, const T (&in)[W]) {
 
 #include "gat_fast.cuh"
 #include "gat_v2.cuh"
+#include "gat_reorder.cuh"
 
 // kernels.hpp:385-423 node_scores: one thread per (node, head), sequential dot
 template <class T>
@@ -807,15 +808,264 @@ static void node_scores_fast(sgnn_ctx ctx, int R, int32_t n, int32_t h, int32_t 
   launched(ctx);
 }
 
+// ---------------------------------------------------------------------------
+// Operator-reordered layer for wide heads (gat_reorder.cuh): every edge
+// gather moves from the k-wide rows of M = X Theta onto the m-wide rows of X
+// (and, in the backward, the h x m rows of Gtheta = G_t Theta_t^T); the
+// per-head transforms run on the tcgen05 GEMM with pitched operands.  Taken
+// when the caller allows it (sgnn_gat_forward_ex SGNN_GAT_REORDER, the Gat2
+// model) and the shape gains: float32, k > m, h in {1,2,4,8}, m and k
+// multiples of 4, the h x m Gtheta row fits a warp's registers, no hub rows.
+// SGNN_GAT_REORDER=0 turns it off (A/B switch).
+// ---------------------------------------------------------------------------
+#define REO_H(H_, ...)                                               \
+  switch (H_) {                                                      \
+    case 1: { constexpr int HH = 1; __VA_ARGS__; } break;            \
+    case 2: { constexpr int HH = 2; __VA_ARGS__; } break;            \
+    case 4: { constexpr int HH = 4; __VA_ARGS__; } break;            \
+    case 8: { constexpr int HH = 8; __VA_ARGS__; } break;            \
+    default: throw std::logic_error("gat reorder: unsupported head count"); \
+  }
+#define REO_HRM(H_, RM_, ...)                                                      \
+  switch ((H_) * 8 + (RM_)) {                                                      \
+    case 1 * 8 + 1: { constexpr int HH = 1, RM = 1; __VA_ARGS__; } break;          \
+    case 1 * 8 + 2: { constexpr int HH = 1, RM = 2; __VA_ARGS__; } break;          \
+    case 1 * 8 + 3: { constexpr int HH = 1, RM = 3; __VA_ARGS__; } break;          \
+    case 1 * 8 + 4: { constexpr int HH = 1, RM = 4; __VA_ARGS__; } break;          \
+    case 2 * 8 + 1: { constexpr int HH = 2, RM = 1; __VA_ARGS__; } break;          \
+    case 2 * 8 + 2: { constexpr int HH = 2, RM = 2; __VA_ARGS__; } break;          \
+    case 2 * 8 + 3: { constexpr int HH = 2, RM = 3; __VA_ARGS__; } break;          \
+    case 2 * 8 + 4: { constexpr int HH = 2, RM = 4; __VA_ARGS__; } break;          \
+    case 4 * 8 + 1: { constexpr int HH = 4, RM = 1; __VA_ARGS__; } break;          \
+    case 4 * 8 + 2: { constexpr int HH = 4, RM = 2; __VA_ARGS__; } break;          \
+    case 4 * 8 + 3: { constexpr int HH = 4, RM = 3; __VA_ARGS__; } break;          \
+    case 4 * 8 + 4: { constexpr int HH = 4, RM = 4; __VA_ARGS__; } break;          \
+    case 8 * 8 + 1: { constexpr int HH = 8, RM = 1; __VA_ARGS__; } break;          \
+    case 8 * 8 + 2: { constexpr int HH = 8, RM = 2; __VA_ARGS__; } break;          \
+    default: throw std::logic_error("gat reorder: unsupported shape");            \
+  }
+
+static bool reorder_env_off() {
+  static const bool off = [] {
+    const char* e = getenv("SGNN_GAT_REORDER");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
+static int reo_rm(int32_t m) { return (int)ceil_div(m / 4, 32); }
+
+static bool reorder_shape_ok(int32_t n, int32_t m, int32_t h, int32_t k) {
+  if (reorder_env_off() || !gemm_tc_available() || n <= 0) return false;
+  if (!(h == 1 || h == 2 || h == 4 || h == 8)) return false;
+  if (k <= m || (m & 3) || (k & 3)) return false;
+  const int RM = reo_rm(m);
+  return RM <= 4 && h * RM <= 16;
+}
+
+// W = [Theta_t a_src_t ; Theta_t a_dst_t] (2 x h x m)
+static void reo_wvec(sgnn_ctx ctx, int32_t m, int32_t h, int32_t k, const float* theta,
+                     const float* a_src, const float* a_dst, float* W) {
+  g2::k_gat_wvec<<<(unsigned)ceil_div(2LL * h * m, 8), 256, 0, ctx->stream>>>(m, h, k, theta,
+                                                                              a_src, a_dst, W);
+  launched(ctx);
+}
+
+static void reo_scores(sgnn_ctx ctx, int32_t n, int32_t m, int32_t h, const float* X,
+                       const float* W, float* s, float* d) {
+  const int32_t mv = m / 4;
+  const size_t smem = (size_t)2 * h * mv * sizeof(float4);
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const float4* W4 = reinterpret_cast<const float4*>(W);
+  REO_HRM(h, reo_rm(m), (g2::k_gat_xscores<HH, RM><<<v2_grid(n), 256, smem, ctx->stream>>>(
+                            n, mv, X4, W4, s, d)));
+  launched(ctx);
+}
+
+// alpha (and mask) of the reordered layer from the scores (k_gat_attn4)
+static void reo_attention(sgnn_ctx ctx, sgnn_pattern p, int32_t h, float beta, const float* s,
+                          const float* d, float* alpha, uint8_t* mask) {
+  const int32_t n = p->n;
+  REO_H(h, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, ctx->stream>>>(
+               n, p->rowptr.as<int32_t>(), p->cols.as<int32_t>(), s, d, beta, alpha, mask,
+               0x7fffffff)));
+  launched(ctx);
+}
+
+static void reo_aggregate(sgnn_ctx ctx, sgnn_pattern p, int32_t m, int32_t h, const float* alpha,
+                          const float* X, float* Z) {
+  const int32_t n = p->n, mv = m / 4;
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  float4* Z4 = reinterpret_cast<float4*>(Z);
+  REO_HRM(h, reo_rm(m), (g2::k_gat_aggx<HH, RM><<<v2_grid(n), 256, 0, ctx->stream>>>(
+                            n, p->rowptr.as<int32_t>(), p->cols.as<int32_t>(), alpha, X4, mv, Z4)));
+  launched(ctx);
+}
+
+static void reo_gemm(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
+                     const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
+                     float* C, int32_t ldc, const float* bias) {
+  if (!gemm_tc_f32_pitched(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias))
+    throw std::runtime_error("gat reorder: pitched tcgen05 GEMM rejected its operands");
+}
+
+static void gat_forward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* X, int32_t m,
+                                  const float* theta, const float* a_src, const float* a_dst,
+                                  const float* bias, int32_t h, int32_t k, float beta, int level,
+                                  float* out, sgnn_gat_cache c) {
+  const int32_t n = p->n, hk = h * k, hm = h * m;
+  const int64_t q = p->nnz;
+  cudaStream_t st = ctx->stream;
+  DevBuf W((size_t)2 * hm * 4, st), s((size_t)n * h * 4 + 16, st), d((size_t)n * h * 4 + 16, st),
+      Z((size_t)n * hm * 4, st), alpha((size_t)q * h * 4 + 16, st), mask;
+  if (level == SGNN_GAT_FULL) mask = DevBuf((size_t)q * h + 16, st);
+  reo_wvec(ctx, m, h, k, theta, a_src, a_dst, W.as<float>());
+  reo_scores(ctx, n, m, h, X, W.as<float>(), s.as<float>(), d.as<float>());
+  reo_attention(ctx, p, h, beta, s.as<float>(), d.as<float>(), alpha.as<float>(),
+                mask.as<uint8_t>());
+  reo_aggregate(ctx, p, m, h, alpha.as<float>(), X, Z.as<float>());
+  for (int32_t t = 0; t < h; ++t)  // out_t = Z_t Theta_t + b_t
+    reo_gemm(ctx, Z.as<float>() + (size_t)t * m, n, m, hm, theta + (size_t)t * k, m, k, hk,
+             false, false, out + (size_t)t * k, hk, bias + (size_t)t * k);
+  c->reordered = true;
+  c->saved_input = X;
+  c->q = q;
+  if (level >= SGNN_GAT_FEATURES) {
+    c->Z = std::move(Z);
+    c->Z.track(kCache, (size_t)n * hm * 4);
+  }
+  if (level == SGNN_GAT_NODE_ATTENTION) {
+    c->s = std::move(s);
+    c->d = std::move(d);
+    c->s.track(kCache, (size_t)n * h * 4);
+    c->d.track(kCache, (size_t)n * h * 4);
+  }
+  if (level == SGNN_GAT_FULL) {
+    c->alpha = std::move(alpha);
+    c->mask = std::move(mask);
+    c->alpha.track(kCache, (size_t)q * h * 4);
+    c->mask.track(kCache, (size_t)q * h);
+  }
+}
+
+// alpha / mask of a reordered cache (kept at level full, else recomputed from
+// the kept or recomputed scores)
+struct ReoEdges {
+  DevBuf alpha, mask, s, d;
+  const float* a = nullptr;
+  const uint8_t* mk = nullptr;
+};
+static void reo_edges(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const float* W,
+                      ReoEdges& r) {
+  const int32_t n = p->n, h = c->h;
+  const int64_t q = p->nnz;
+  cudaStream_t st = ctx->stream;
+  if (c->level == SGNN_GAT_FULL) {
+    r.a = c->alpha.as<float>();
+    r.mk = c->mask.as<uint8_t>();
+    return;
+  }
+  const float *sp, *dp;
+  if (c->level == SGNN_GAT_NODE_ATTENTION) {
+    sp = c->s.as<float>();
+    dp = c->d.as<float>();
+  } else {
+    r.s = DevBuf((size_t)n * h * 4 + 16, st);
+    r.d = DevBuf((size_t)n * h * 4 + 16, st);
+    reo_scores(ctx, n, c->m, h, static_cast<const float*>(c->saved_input), W, r.s.as<float>(),
+               r.d.as<float>());
+    sp = r.s.as<float>();
+    dp = r.d.as<float>();
+  }
+  r.alpha = DevBuf((size_t)q * h * 4 + 16, st);
+  r.mask = DevBuf((size_t)q * h + 16, st);
+  reo_attention(ctx, p, h, (float)c->beta, sp, dp, r.alpha.as<float>(), r.mask.as<uint8_t>());
+  r.a = r.alpha.as<float>();
+  r.mk = r.mask.as<uint8_t>();
+}
+
+static void gat_backward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* G,
+                                   const float* theta, const float* a_src, const float* a_dst,
+                                   sgnn_gat_cache c, bool fg, float* d_theta, float* d_a_src,
+                                   float* d_a_dst, float* d_bias, float* d_input) {
+  const int32_t n = p->n, h = c->h, k = c->k, m = c->m, hk = h * k, hm = h * m, mv = m / 4;
+  const int RM = reo_rm(m);
+  const int64_t q = p->nnz;
+  const float* X = static_cast<const float*>(c->saved_input);
+  cudaStream_t st = ctx->stream;
+  const int32_t* rp = p->rowptr.as<int32_t>();
+  const int32_t* ci = p->cols.as<int32_t>();
+  DevBuf W((size_t)2 * hm * 4, st);
+  reo_wvec(ctx, m, h, k, theta, a_src, a_dst, W.as<float>());
+  ReoEdges e;
+  reo_edges(ctx, p, c, W.as<float>(), e);
+  DevBuf Zt;
+  const float* Z;
+  if (c->level >= SGNN_GAT_FEATURES) {
+    Z = c->Z.as<float>();
+  } else {
+    Zt = DevBuf((size_t)n * hm * 4, st);
+    reo_aggregate(ctx, p, m, h, e.a, X, Zt.as<float>());
+    Z = Zt.as<float>();
+  }
+  // Gtheta_t = G_t Theta_t^T  (n x h x m)
+  DevBuf Gt((size_t)n * hm * 4, st);
+  for (int32_t t = 0; t < h; ++t)
+    reo_gemm(ctx, G + (size_t)t * k, n, k, hk, theta + (size_t)t * k, m, k, hk, false, true,
+             Gt.as<float>() + (size_t)t * m, hm, nullptr);
+  // dAlpha, then the softmax / LeakyReLU backward (k_gat_sbwd4: dy, dS)
+  DevBuf da((size_t)q * h * 4 + 16, st), dy((size_t)q * h * 4 + 16, st),
+      dS((size_t)n * h * 4 + 16, st), dD((size_t)n * h * 4 + 16, st);
+  const float4* X4 = reinterpret_cast<const float4*>(X);
+  const float4* Gt4 = reinterpret_cast<const float4*>(Gt.get());
+  REO_HRM(h, RM, (g2::k_gat_sddmmx<HH, RM><<<v2_grid(n), 256, 0, st>>>(n, rp, ci, Gt4, X4, mv,
+                                                                       da.as<float>())));
+  launched(ctx);
+  REO_H(h, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
+               n, rp, e.a, e.mk, da.as<float>(), (float)c->beta, dy.as<float>(), dS.as<float>())));
+  launched(ctx);
+  const int32_t* cp = p->colptr.as<int32_t>();
+  const int32_t* pm = p->perm.as<int32_t>();
+  if (fg) {  // d_input and dD in one column pass
+    REO_HRM(h, RM, (g2::k_gat_colx<HH, RM><<<v2_grid(n), 256, 0, st>>>(
+                       n, cp, p->rows.as<int32_t>(), pm, Gt4, e.a, dy.as<float>(), dS.as<float>(),
+                       reinterpret_cast<const float4*>(W.get()), mv, dD.as<float>(),
+                       reinterpret_cast<float4*>(d_input))));
+  } else {
+    REO_H(h, (g2::k_gat_colsum_dy<HH><<<v2_grid(n), 256, 0, st>>>(n, cp, pm, dy.as<float>(),
+                                                                  dD.as<float>())));
+  }
+  launched(ctx);
+  // U_S = X^T dS, U_D = X^T dD (m x h); dTheta_t = Z_t^T G_t + rank-1 terms
+  DevBuf us((size_t)m * h * 4 + 16, st), ud((size_t)m * h * 4 + 16, st);
+  gemm<float>(ctx, X, n, m, dS.as<float>(), n, h, true, false, us.as<float>());
+  gemm<float>(ctx, X, n, m, dD.as<float>(), n, h, true, false, ud.as<float>());
+  for (int32_t t = 0; t < h; ++t)
+    reo_gemm(ctx, Z + (size_t)t * m, n, m, hm, G + (size_t)t * k, n, k, hk, true, false,
+             d_theta + (size_t)t * k, hk, nullptr);
+  g2::k_gat_reorder_grads<<<(unsigned)ceil_div(hk, 256), 256, 0, st>>>(
+      m, h, k, theta, a_src, a_dst, us.as<float>(), ud.as<float>(), d_theta, d_a_src, d_a_dst);
+  launched(ctx);
+  column_sums<float>(ctx, G, n, hk, d_bias);
+}
+
 template <class T>
 void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T* theta,
                    const T* a_src, const T* a_dst, const T* bias, int32_t h, int32_t k,
                    T beta, int level, T* out, sgnn_gat_cache c, uint8_t* elu_mask = nullptr,
-                   bool* elu_fused = nullptr) {
+                   bool* elu_fused = nullptr, bool reorder = false) {
   const int32_t n = p->n;
   const int64_t q = p->nnz;
   const int32_t hk = h * k;
   cudaStream_t st = ctx->stream;
+  if constexpr (sizeof(T) == 4) {
+    if (reorder && reorder_shape_ok(n, m, h, k) && al16(X) && al16(theta) && al16(a_src) &&
+        al16(a_dst) && al16(bias) && al16(out) &&
+        long_rows(ctx, p->long_rows, n, p->rowptr.as<int32_t>()).nlong == 0) {
+      gat_forward_reordered(ctx, p, X, m, theta, a_src, a_dst, bias, h, k, beta, level, out, c);
+      return;
+    }
+  }
   DevBuf M((size_t)n * hk * sizeof(T), st), s((size_t)n * h * sizeof(T) + 8, st),
       d((size_t)n * h * sizeof(T) + 8, st), alpha, mask;
   const int32_t* rp = p->rowptr.as<int32_t>();
@@ -1001,6 +1251,13 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     }
     gemm<T>(ctx, dM, c->n, c->h * c->k, theta, c->m, c->h * c->k, false, true, d_input);
   };
+  if constexpr (sizeof(T) == 4) {
+    if (c->reordered) {
+      gat_backward_reordered(ctx, p, G, theta, a_src, a_dst, c, fg, d_theta, d_a_src, d_a_dst,
+                             d_bias, d_input);
+      return;
+    }
+  }
   const int32_t n = p->n, h = c->h, k = c->k, hk = h * k, m = c->m;
   const int64_t q = p->nnz;
   const T beta = (T)c->beta;
@@ -1208,6 +1465,18 @@ void gat_edge_values_t(sgnn_ctx ctx, sgnn_pattern p, sgnn_gat_cache c, const T* 
   DevBuf al, mk;
   const T* ae;
   const uint8_t* me;
+  if constexpr (sizeof(T) == 4) {
+    if (c->reordered) {
+      DevBuf W((size_t)2 * h * c->m * 4, st);
+      reo_wvec(ctx, c->m, h, k, theta, a_src, a_dst, W.as<float>());
+      ReoEdges e;
+      reo_edges(ctx, p, c, W.as<float>(), e);
+      k_edge_to_head_major<T><<<grid_for(ctx, q * h, 256), 256, 0, st>>>(q, h, e.a, e.mk,
+                                                                         alpha_hq, mask_hq);
+      launched(ctx);
+      return;
+    }
+  }
   if (c->level == SGNN_GAT_FULL) {
     ae = c->alpha.as<T>();
     me = c->mask.as<uint8_t>();
@@ -1238,7 +1507,26 @@ int sgnn_gat_forward(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, con
                      int32_t k, double beta, int level, int dtype, void* out,
                      sgnn_gat_cache* cache) {
   return sgnn::gat_forward_elu(ctx, p, X, m, theta, a_src, a_dst, bias, heads, k, beta, level,
-                               dtype, out, cache, nullptr, nullptr);
+                               dtype, out, cache, nullptr, nullptr, false);
+}
+
+int sgnn_gat_forward_ex(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
+                        const void* a_src, const void* a_dst, const void* bias, int32_t heads,
+                        int32_t k, double beta, int level, int dtype, void* out,
+                        sgnn_gat_cache* cache, int flags) {
+  if (flags & ~SGNN_GAT_REORDER) {
+    set_last_error("gat_forward_ex: unknown flags");
+    return SGNN_EINVAL;
+  }
+  return sgnn::gat_forward_elu(ctx, p, X, m, theta, a_src, a_dst, bias, heads, k, beta, level,
+                               dtype, out, cache, nullptr, nullptr, (flags & SGNN_GAT_REORDER) != 0);
+}
+
+int sgnn_gat_cache_reordered(sgnn_gat_cache c, int* out) {
+  SGNN_API_BEGIN
+  require(c != nullptr && out != nullptr, "gat cache: null argument");
+  *out = c->reordered ? 1 : 0;
+  SGNN_API_END
 }
 
 int sgnn_gat_backward(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
@@ -1256,7 +1544,7 @@ int sgnn::gat_forward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m
                           const void* theta, const void* a_src, const void* a_dst,
                           const void* bias, int32_t heads, int32_t k, double beta, int level,
                           int dtype, void* out, sgnn_gat_cache* cache, uint8_t* elu_mask,
-                          bool* fused) {
+                          bool* fused, bool reorder) {
   if (fused) *fused = false;
   SGNN_API_BEGIN
   require(p && p->all_self_loops, "gat_forward: pattern must contain all self loops");
@@ -1276,7 +1564,7 @@ int sgnn::gat_forward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m
     if (dtype == SGNN_F32)
       gat_forward_t<float>(ctx, p, (const float*)X, m, (const float*)theta, (const float*)a_src,
                            (const float*)a_dst, (const float*)bias, heads, k, (float)beta, level,
-                           (float*)out, c, elu_mask, fused);
+                           (float*)out, c, elu_mask, fused, reorder);
     else if (dtype == SGNN_F64)
       gat_forward_t<double>(ctx, p, (const double*)X, m, (const double*)theta,
                             (const double*)a_src, (const double*)a_dst, (const double*)bias,
@@ -1305,7 +1593,8 @@ int sgnn::gat_backward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, cons
           "gat_backward: gradient shape mismatch");
   require(c->saved_input != nullptr && m == c->m, "gat_backward: missing saved input");
   if (c->level >= SGNN_GAT_FEATURES)
-    require(c->M.get() != nullptr, "gat_backward: cache level promises M but it is absent");
+    require((c->reordered ? c->Z.get() : c->M.get()) != nullptr,
+            "gat_backward: cache level promises M but it is absent");
   if (c->level == SGNN_GAT_FULL)
     require(c->alpha.get() != nullptr && c->mask.get() != nullptr,
             "gat_backward: cache level promises alpha/mask but they are absent");
@@ -1352,6 +1641,7 @@ int sgnn_gat_cache_extra_bytes(sgnn_gat_cache c, int64_t* out) {
   const int64_t sb = c->dtype == SGNN_F32 ? 4 : 8;
   int64_t b = 0;
   if (c->M.get()) b += sb * c->n * c->h * c->k;
+  if (c->Z.get()) b += sb * c->n * c->h * c->m;  // reordered layer: Z in place of M
   if (c->s.get()) b += 2 * sb * c->n * c->h;
   if (c->alpha.get()) b += (sb + 1) * c->q * c->h;
   *out = b;

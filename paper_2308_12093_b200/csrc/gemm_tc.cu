@@ -199,6 +199,19 @@ __global__ void k_split_global(int64_t n, const float* __restrict__ x, float* __
   }
 }
 
+// the same for a rows x cols block of a matrix with row pitch ld (contiguous out)
+__global__ void k_split_global2d(int32_t rows, int32_t cols, const float* __restrict__ x,
+                                 int32_t ld, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[(i / cols) * ld + i % cols];
+    const float h = __uint_as_float(tf32_hi(v));
+    hi[i] = h;
+    lo[i] = __fsub_rn(v, h);
+  }
+}
+
 // optional epilogue: GAT node scores s = M a_src^T, d = M a_dst^T per head
 // (kernels.hpp:385-423) from the output tile while it is in registers
 struct EpiScores {
@@ -221,6 +234,8 @@ struct EpiScores {
   // accumulations per k-block into one growing sum (5e-6 relative bias at
   // K = 500, measured); the final sum goes back to TMEM for the epilogue
   bool drain = false;
+  // row pitch of C in elements (0: N) -- column blocks of a wider matrix
+  int ldc = 0;
 };
 
 template <int BN>
@@ -900,8 +915,8 @@ static void launch(sgnn_ctx ctx, const Maps& mp, int M, int N, int K, int splits
   const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * splits;
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
   kern<<<grid, NUM_THREADS, smem, ctx->stream>>>(mp.a, mp.b, mp.blo, mp.c, M, N, K, kchunk,
-                                                  splits, C, N, bias, part, tma_store, cs_part,
-                                                  sc);
+                                                  splits, C, sc.ldc ? sc.ldc : N, bias, part,
+                                                  tma_store, cs_part, sc);
   launched(ctx);
 }
 
@@ -962,6 +977,8 @@ static bool tc_disabled() {
   }
   return v == 1;
 }
+
+bool gemm_tc_available() { return !tc_disabled(); }
 
 // Zero-padded copy of a rows x cols row-major matrix (pitch ld) into an
 // orows x ocols one: TMA needs 16-byte row pitches, so operands whose stored
@@ -1077,18 +1094,50 @@ static bool gemm_tc_f32_padded(sgnn_ctx ctx, const float* A, int32_t ra, int32_t
 // column sums of B over its K rows -- d_bias = 1^T dX' fused into the dTheta
 // GEMM, so dX' is read once.  Returns false without doing anything if the
 // fused form does not apply (the caller then runs the two ops separately).
+static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
+                             const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
+                             float* C, int32_t ldc, const float* bias, float* colsum_b,
+                             const float* att_src, const float* att_dst, float* s_out,
+                             float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
+                             const float* elu_saved);
+
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                  float* colsum_b, const float* att_src, const float* att_dst, float* s_out,
                  float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
                  const float* elu_saved) {
+  return gemm_tc_f32_impl(ctx, A, ra, ca, ca, B, rb, cb, cb, ta, tb, C, 0, bias, colsum_b,
+                          att_src, att_dst, s_out, d_out, heads, relu_out, mask_in, elu_saved);
+}
+
+// C = op(A) op(B) (+ bias) on blocks of wider matrices: A, B, C with row
+// pitches lda, ldb, ldc (elements, multiples of 4); e.g. one head's column
+// block of an n x (h k) slab.  false (nothing launched) if not supported.
+bool gemm_tc_f32_pitched(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
+                         const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
+                         float* C, int32_t ldc, const float* bias) {
+  if ((lda & 3) || (ldb & 3) || (ldc & 3)) return false;
+  return gemm_tc_f32_impl(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr);
+}
+
+static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
+                             const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
+                             float* C, int32_t ldc, const float* bias, float* colsum_b,
+                             const float* att_src, const float* att_dst, float* s_out,
+                             float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
+                             const float* elu_saved) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
   if (M <= 0 || N <= 0 || K <= 0) return false;
-  if ((int64_t)M * N * K < (int64_t)1 << 20) return false;  // tiny: SIMT is fine
+  const bool pitched = lda != ca || ldb != cb || (ldc != 0 && ldc != N);
+  // tiny: SIMT is fine (pitched operands have no SIMT path)
+  if (!pitched && (int64_t)M * N * K < (int64_t)1 << 20) return false;
+  if (ldc <= 0) ldc = N;
+  if (pitched && (colsum_b || att_src || relu_out || mask_in || elu_saved)) return false;
   static const bool no_pad = getenv("SGNN_NO_PAD") != nullptr;  // dev switch
-  if ((ca & 3) || (cb & 3)) {  // 16-byte row pitches for TMA: stage padded operands
+  if (!pitched && ((ca & 3) || (cb & 3))) {  // 16-byte row pitches for TMA: stage padded operands
     if (no_pad) return false;
     return gemm_tc_f32_padded(ctx, A, ra, ca, B, rb, cb, ta, tb, C, bias, colsum_b, att_src,
                               att_dst, s_out, d_out, heads, relu_out, mask_in, elu_saved);
@@ -1141,8 +1190,8 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   const float* Blo = B;
   Maps mp;
   // A: ta -> stored K x M (MN-major), else M x K (K-major)
-  const bool okA = a_mn ? make_map(&mp.a, A, M, K, ca, BK, true)
-                        : make_map(&mp.a, A, K, M, ca, BM, false);
+  const bool okA = a_mn ? make_map(&mp.a, A, M, K, lda, BK, true)
+                        : make_map(&mp.a, A, K, M, lda, BM, false);
   if (!okA) return false;
   if (pre) {
     bsplit = DevBuf((size_t)belems * 8, ctx->stream);
@@ -1150,10 +1199,11 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     Blo = bsplit.as<float>() + belems;
   }
   // B: tb -> stored N x K (K-major), else K x N (MN-major)
-  bool okB = b_mn ? make_map(&mp.b, Bhi, N, K, cb, BK, true)
-                  : make_map(&mp.b, Bhi, K, N, cb, BN, false);
-  okB = okB && (b_mn ? make_map(&mp.blo, Blo, N, K, cb, BK, true)
-                     : make_map(&mp.blo, Blo, K, N, cb, BN, false));
+  const int32_t bld = pre ? cb : ldb;  // the pre-split copies are contiguous
+  bool okB = b_mn ? make_map(&mp.b, Bhi, N, K, bld, BK, true)
+                  : make_map(&mp.b, Bhi, K, N, bld, BN, false);
+  okB = okB && (b_mn ? make_map(&mp.blo, Blo, N, K, bld, BK, true)
+                     : make_map(&mp.blo, Blo, K, N, bld, BN, false));
   if (!okB) return false;
   int splits = split_count(BN);
   int kchunk = (int)ceil_div(ceil_div(K, splits), BK) * BK;
@@ -1185,7 +1235,9 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
   if (elu_saved && (!mask_in || (reinterpret_cast<uintptr_t>(elu_saved) & 15))) return false;
   if ((sc.a_src || relu_out || mask_in) && (a_mn || !pre)) return false;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)
-  const int tma_store = (splits == 1 && (N & 3) == 0 && make_map(&mp.c, C, N, M, N, 32, false));
+  sc.ldc = ldc;
+  const int tma_store = (splits == 1 && (N & 3) == 0 && (ldc & 3) == 0 &&
+                         make_map(&mp.c, C, N, M, ldc, 32, false));
   if (!tma_store) mp.c = mp.a;  // unused
   if (relu_out || mask_in) {  // fused ReLU / ReLU backward: TMA-store epilogue, whole 32-col chunks
     if (!tma_store || (N & 31) != 0 || (reinterpret_cast<uintptr_t>(relu_out) & 15) ||
@@ -1193,8 +1245,12 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
       return false;
   }
   if (pre) {
-    k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
-        belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);
+    if (ldb == cb)
+      k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
+          belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);
+    else
+      k_split_global2d<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
+          rb, cb, B, ldb, bsplit.as<float>(), bsplit.as<float>() + belems);
     launched(ctx);
   }
   DevBuf part, csp;
@@ -1219,7 +1275,7 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
     // split-K partials -> C, and the fused column sums in the same launch
     const unsigned ncs = colsum_b ? (unsigned)ceil_div(N, 32) : 0u;
     k_reduce_splits<<<(unsigned)ceil_div(MN, 32) + ncs, 256, 0, ctx->stream>>>(
-        splits, MN, N, pp, C, N, bias, splits * 4, cs, colsum_b);
+        splits, MN, N, pp, C, ldc, bias, splits * 4, cs, colsum_b);
     launched(ctx);
   } else if (colsum_b) {
     k_colsum_parts<<<(unsigned)N, 256, 0, ctx->stream>>>(splits * 4, N, cs, colsum_b);

@@ -68,6 +68,10 @@ struct sgnn_gat_cache_s {
   sgnn::DevBuf M;                     // level >= features
   sgnn::DevBuf s, d;                  // level == node_attention
   sgnn::DevBuf alpha, mask;           // level == full
+  // operator-reordered layer (gat_reorder.cuh): Z = alpha-aggregated input
+  // (n x h x m) in place of M at level >= features
+  bool reordered = false;
+  sgnn::DevBuf Z;
   bool consumed = false;
 };
 
@@ -109,7 +113,8 @@ bool gemm_elu_bwd_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, cons
 int gat_forward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* X, int32_t m, const void* theta,
                     const void* a_src, const void* a_dst, const void* bias, int32_t heads,
                     int32_t k, double beta, int level, int dtype, void* out,
-                    sgnn_gat_cache* cache, uint8_t* elu_mask, bool* fused);
+                    sgnn_gat_cache* cache, uint8_t* elu_mask, bool* fused,
+                    bool reorder = false);
 int gat_backward_elu(sgnn_ctx ctx, sgnn_pattern p, const void* d_out, const void* theta,
                      const void* a_src, const void* a_dst, int32_t m, int32_t heads, int32_t k,
                      sgnn_gat_cache c, int fg, void* d_theta, void* d_a_src, void* d_a_dst,
@@ -134,6 +139,14 @@ template <class T>
 void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t* cols,
               const T* vals, const T* B, int32_t f, T* C, const T* bias, int64_t nnz,
               const LongRows* lr = nullptr, int32_t b_rows = -1);
+
+// tcgen05 GEMM on blocks of wider matrices (row pitches lda / ldb / ldc,
+// multiples of 4 floats); false when the shape is not supported
+// false when SGNN_DISABLE_TCGEN05=1 (A/B switch of the tcgen05 GEMMs)
+bool gemm_tc_available();
+bool gemm_tc_f32_pitched(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
+                         const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
+                         float* C, int32_t ldc, const float* bias);
 
 // row-padded staging copies of float32 matrices (gemm_tc.cu): zero-padded to
 // ocols columns / back to ocols columns with an optional bias add

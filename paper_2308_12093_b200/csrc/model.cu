@@ -190,10 +190,12 @@ void gat2_step(sgnn_ctx ctx, sgnn_model md, sgnn_pattern P, const T* X, const T*
   bool fused = false;
   ok(gat_forward_elu(ctx, P, X, m, prm(0), prm(1), prm(2), prm(3), hd, hid, beta, cf.gat_level,
                      md->dtype, h.get(), &c1.c, act_fusion() ? mask.as<uint8_t>() : nullptr,
-                     &fused));
+                     &fused, true));
   if (!fused) act_fwd<T>(ctx, 2, (int64_t)n * w1, h.as<T>(), h.as<T>(), mask.as<uint8_t>());
-  ok(sgnn_gat_forward(ctx, P, h.get(), w1, prm(4), prm(5), prm(6), prm(7), hd, k, beta,
-                      cf.gat_level, md->dtype, o, &c2.c));
+  // both layers may run operator-reordered (wide heads, k > m): the model
+  // keeps its caches private, so only its outputs and gradients are visible
+  ok(sgnn_gat_forward_ex(ctx, P, h.get(), w1, prm(4), prm(5), prm(6), prm(7), hd, k, beta,
+                         cf.gat_level, md->dtype, o, &c2.c, SGNN_GAT_REORDER));
   DevBuf g((size_t)n * w2 * sizeof(T), st), dl(sizeof(double), st);
   mse<T>(ctx, (int64_t)n * w2, o, target, g.as<T>(), loss ? loss : dl.as<double>());
   DevBuf dh((size_t)n * w1 * sizeof(T), st);

@@ -558,6 +558,13 @@ class GatCache:
         check(lib.sgnn_gat_cache_extra_bytes(self.handle, C.byref(v)))
         return v.value
 
+    @property
+    def reordered(self):
+        """True when the forward ran operator-reordered (gat_forward reorder=True)."""
+        v = C.c_int()
+        check(lib.sgnn_gat_cache_reordered(self.handle, C.byref(v)))
+        return bool(v.value)
+
     def edge_values(self, pattern: Pattern, theta, a_src, a_dst):
         """alpha (h x q) and mask (h x q uint8), head-major like the reference."""
         dev = pattern.ctx.device
@@ -575,7 +582,11 @@ class GatCache:
 
 
 def gat_forward(pattern: Pattern, X, theta, a_src, a_dst, bias, heads, beta=0.2,
-                level="none", out=None):
+                level="none", out=None, reorder=False):
+    """One GAT layer forward (gat.hpp:89-147).  reorder=True lets the device
+    run it operator-reordered when the heads are wider than the input (k > m,
+    float32; sgnn_gat_forward_ex): same outputs and gradients within float32
+    rounding, the cache keeps Z = sum_j alpha X_j in place of M."""
     X, theta = X.contiguous(), theta.contiguous()
     a_src, a_dst, bias = a_src.contiguous(), a_dst.contiguous(), bias.contiguous()
     if isinstance(level, str):
@@ -593,9 +604,10 @@ def gat_forward(pattern: Pattern, X, theta, a_src, a_dst, bias, heads, beta=0.2,
     if out is None:
         out = torch.empty((n, hk), dtype=X.dtype, device=X.device)
     h = C.c_void_p()
-    check(lib.sgnn_gat_forward(pattern.ctx.handle, pattern.handle, _p(X), m, _p(theta),
-                               _p(a_src), _p(a_dst), _p(bias), heads, k, float(beta), int(level),
-                               _dt(X), _p(out), C.byref(h)))
+    check(lib.sgnn_gat_forward_ex(pattern.ctx.handle, pattern.handle, _p(X), m, _p(theta),
+                                  _p(a_src), _p(a_dst), _p(bias), heads, k, float(beta),
+                                  int(level), _dt(X), _p(out), C.byref(h),
+                                  _c.GAT_REORDER if reorder else 0))
     return out, GatCache(h, X, level, heads, k)
 
 
