@@ -904,15 +904,16 @@ static void reo_aggregate(sgnn_ctx ctx, sgnn_pattern p, int32_t m, int32_t h, co
 
 static void reo_gemm(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
                      const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
-                     float* C, int32_t ldc, const float* bias) {
-  if (!gemm_tc_f32_pitched(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias))
+                     float* C, int32_t ldc, const float* bias, float* colsum_b = nullptr) {
+  if (!gemm_tc_f32_pitched(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias, colsum_b))
     throw std::runtime_error("gat reorder: pitched tcgen05 GEMM rejected its operands");
 }
 
 static void gat_forward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* X, int32_t m,
                                   const float* theta, const float* a_src, const float* a_dst,
                                   const float* bias, int32_t h, int32_t k, float beta, int level,
-                                  float* out, sgnn_gat_cache c) {
+                                  float* out, sgnn_gat_cache c, uint8_t* elu_mask,
+                                  bool* elu_fused) {
   const int32_t n = p->n, hk = h * k, hm = h * m;
   const int64_t q = p->nnz;
   cudaStream_t st = ctx->stream;
@@ -924,9 +925,25 @@ static void gat_forward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* X, 
   reo_attention(ctx, p, h, beta, s.as<float>(), d.as<float>(), alpha.as<float>(),
                 mask.as<uint8_t>());
   reo_aggregate(ctx, p, m, h, alpha.as<float>(), X, Z.as<float>());
-  for (int32_t t = 0; t < h; ++t)  // out_t = Z_t Theta_t + b_t
-    reo_gemm(ctx, Z.as<float>() + (size_t)t * m, n, m, hm, theta + (size_t)t * k, m, k, hk,
-             false, false, out + (size_t)t * k, hk, bias + (size_t)t * k);
+  // out_t = Z_t Theta_t + b_t, with the caller's ELU(1) in the epilogue when
+  // the heads are whole 32-column chunks (the first head decides; all share
+  // shape, pitch and alignment)
+  bool fuse = elu_mask != nullptr;
+  for (int32_t t = 0; t < h; ++t) {
+    const float* A = Z.as<float>() + (size_t)t * m;
+    const float* B = theta + (size_t)t * k;
+    float* C = out + (size_t)t * k;
+    if (fuse) {
+      if (gemm_tc_f32_pitched(ctx, A, n, m, hm, B, m, k, hk, false, false, C, hk,
+                              bias + (size_t)t * k, nullptr, elu_mask + (size_t)t * k)) {
+        if (elu_fused) *elu_fused = true;
+        continue;
+      }
+      if (t > 0) throw std::logic_error("gat reorder: ELU epilogue rejected after head 0");
+      fuse = false;
+    }
+    reo_gemm(ctx, A, n, m, hm, B, m, k, hk, false, false, C, hk, bias + (size_t)t * k);
+  }
   c->reordered = true;
   c->saved_input = X;
   c->q = q;
@@ -1040,13 +1057,13 @@ static void gat_backward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* G,
   DevBuf us((size_t)m * h * 4 + 16, st), ud((size_t)m * h * 4 + 16, st);
   gemm<float>(ctx, X, n, m, dS.as<float>(), n, h, true, false, us.as<float>());
   gemm<float>(ctx, X, n, m, dD.as<float>(), n, h, true, false, ud.as<float>());
+  // d_bias = 1^T G fused into the dTheta GEMMs (column sums of their B = G_t)
   for (int32_t t = 0; t < h; ++t)
     reo_gemm(ctx, Z + (size_t)t * m, n, m, hm, G + (size_t)t * k, n, k, hk, true, false,
-             d_theta + (size_t)t * k, hk, nullptr);
-  g2::k_gat_reorder_grads<<<(unsigned)ceil_div(hk, 256), 256, 0, st>>>(
+             d_theta + (size_t)t * k, hk, nullptr, d_bias + (size_t)t * k);
+  g2::k_gat_reorder_grads<<<dim3((unsigned)ceil_div(hk, 32)), 256, 0, st>>>(
       m, h, k, theta, a_src, a_dst, us.as<float>(), ud.as<float>(), d_theta, d_a_src, d_a_dst);
   launched(ctx);
-  column_sums<float>(ctx, G, n, hk, d_bias);
 }
 
 template <class T>
@@ -1062,7 +1079,8 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
     if (reorder && reorder_shape_ok(n, m, h, k) && al16(X) && al16(theta) && al16(a_src) &&
         al16(a_dst) && al16(bias) && al16(out) &&
         long_rows(ctx, p->long_rows, n, p->rowptr.as<int32_t>()).nlong == 0) {
-      gat_forward_reordered(ctx, p, X, m, theta, a_src, a_dst, bias, h, k, beta, level, out, c);
+      gat_forward_reordered(ctx, p, X, m, theta, a_src, a_dst, bias, h, k, beta, level, out, c,
+                            elu_mask, elu_fused);
       return;
     }
   }

@@ -301,9 +301,11 @@ __global__ void __launch_bounds__(256) k_gat_colx(int32_t n, const int32_t* __re
 }
 
 // Attention-parameter gradients and the rank-1 terms of dTheta from
-// U = [X^T dS | X^T dD] (m x h each): thread per column c of h k,
+// U = [X^T dS | X^T dD] (m x h each), t = c / k for column c of h k:
 //   d a_src[c] = sum_v U_S[v][t] Theta[v][c],  d a_dst[c] likewise,
-//   dTheta[v][c] += U_S[v][t] a_src[c] + U_D[v][t] a_dst[c]      (t = c / k)
+//   dTheta[v][c] += U_S[v][t] a_src[c] + U_D[v][t] a_dst[c]
+// Block per 32 columns: 8 warps split the m rows (lane = column, coalesced),
+// the per-warp float64 partials of the two dots summed in fixed order.
 __global__ void __launch_bounds__(256) k_gat_reorder_grads(int32_t m, int32_t h, int32_t k,
                                                            const float* __restrict__ theta,
                                                            const float* __restrict__ a_src,
@@ -313,22 +315,32 @@ __global__ void __launch_bounds__(256) k_gat_reorder_grads(int32_t m, int32_t h,
                                                            float* __restrict__ d_theta,
                                                            float* __restrict__ d_a_src,
                                                            float* __restrict__ d_a_dst) {
+  __shared__ double part[2][8][32];
   const int32_t hk = h * k;
-  const int32_t c = (int32_t)(blockIdx.x * 256u + threadIdx.x);
-  if (c >= hk) return;
-  const int32_t t = c / k;
-  const float as = __ldg(a_src + c), ad = __ldg(a_dst + c);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t c = (int32_t)blockIdx.x * 32 + lane;
   double gs = 0.0, gd = 0.0;
-  for (int32_t v = 0; v < m; ++v) {
-    const float uS = __ldg(us + (int64_t)v * h + t), uD = __ldg(ud + (int64_t)v * h + t);
-    const float th = __ldg(theta + (int64_t)v * hk + c);
-    gs += (double)uS * th;
-    gd += (double)uD * th;
-    float* o = d_theta + (int64_t)v * hk + c;
-    *o = fmaf(uD, ad, fmaf(uS, as, *o));
+  if (c < hk) {
+    const int32_t t = c / k;
+    const float as = __ldg(a_src + c), ad = __ldg(a_dst + c);
+    for (int32_t v = w; v < m; v += 8) {
+      const float uS = __ldg(us + (int64_t)v * h + t), uD = __ldg(ud + (int64_t)v * h + t);
+      const float th = __ldg(theta + (int64_t)v * hk + c);
+      gs += (double)uS * th;
+      gd += (double)uD * th;
+      float* o = d_theta + (int64_t)v * hk + c;
+      *o = fmaf(uD, ad, fmaf(uS, as, *o));
+    }
   }
-  d_a_src[c] = (float)gs;
-  d_a_dst[c] = (float)gd;
+  part[0][w][lane] = gs;
+  part[1][w][lane] = gd;
+  __syncthreads();
+  if (w < 2 && c < hk) {
+    double tot = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += part[w][q][lane];
+    (w == 0 ? d_a_src : d_a_dst)[c] = (float)tot;
+  }
 }
 
 }  // namespace g2

@@ -134,6 +134,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tcgen05.ld without the wait: the registers are written asynchronously until
+// tmem_wait32 on the same array, whose "+r" operands keep every use after it
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -228,6 +254,9 @@ struct EpiScores {
   // ELU(1) backward (dense.hpp:232-268) with mask_in: out = mask ? out :
   // (saved + 1) * out, saved = the activation's forward output (row-major n x N)
   const float* elu_saved = nullptr;
+  // with relu_out: ELU(1) forward instead of ReLU -- out = x > 0 ? x : exp(x) - 1
+  // and mask = (x > 0), the expressions of the separate activation pass (EPI bit 5)
+  bool elu = false;
   // k-block drain mode (K > 256, BN <= 128): every k-block is accumulated
   // afresh in one of three TMEM accumulators and added into fp32 registers
   // by the epilogue (round-to-nearest), instead of ~12 truncating tensor-core
@@ -575,12 +604,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int col = n0 + cc;
         const bool ok = row < M && col < N;
         if (EPI & 4) {
-          const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * N + col);
+          const uint4* mp = reinterpret_cast<const uint4*>(sc.mask_in + (int64_t)row * sc.ldc + col);
           mk_n[0] = ok ? __ldg(mp) : make_uint4(0, 0, 0, 0);
           mk_n[1] = ok ? __ldg(mp + 1) : make_uint4(0, 0, 0, 0);
         }
         if (EPI & 16) {
-          const float4* sp = reinterpret_cast<const float4*>(sc.elu_saved + (int64_t)row * N + col);
+          const float4* sp = reinterpret_cast<const float4*>(sc.elu_saved + (int64_t)row * sc.ldc + col);
 #pragma unroll
           for (int j = 0; j < NSV; ++j) sv_n[j] = ok ? __ldg(sp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -635,11 +664,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       float ss = 0.f, sd = 0.f;  // fused node scores of the current head
       int hrem = sc.k >> 2, head = (EPI & 8) ? n0 / sc.k : 0;
+      // software pipeline over the 32-column chunks: the TMEM load of chunk
+      // c + 32 (and lane j's bias of its column j) is in flight while chunk c
+      // is processed, and the accumulator goes back to the MMA warp as soon as
+      // its last chunk is in registers
+      const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN);
+      const float* bsh = (tma_store && !part) ? bias : nullptr;  // bias by shuffle
+      // (not with the ELU backward's saved-value prefetch: registers would spill)
+      constexpr bool PIPE = (EPI & 16) == 0;
+      uint32_t rn[32];
+      if constexpr (PIPE) tmem_ld32_async(tacc, rn);
+      float bnx = (bsh && n0 + lane < N) ? __ldg(bsh + n0 + lane) : 0.f;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         uint4 mk[2];
         float4 sv[NSV];
+        if constexpr (PIPE) {
+          tmem_wait32(rn);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = rn[j];
+        } else {
+          tmem_ld32(tacc + c, r);
+        }
+        const float bcur = bnx;
+        if (c + 32 < BN) {
+          if constexpr (PIPE) tmem_ld32_async(tacc + c + 32, rn);
+          if (bsh) bnx = (n0 + c + 32 + lane < N) ? __ldg(bsh + n0 + c + 32 + lane) : 0.f;
+        } else {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[abuf]);
+        }
         if (EPI & 20) {
           mk[0] = mk_n[0];
           mk[1] = mk_n[1];
@@ -647,7 +703,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < NSV; ++j) sv[j] = sv_n[j];
           if (c + 32 < BN) fetch(c + 32);
         }
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN + c), r);
         if ((EPI & 1) && n0 + c < N) {
           // s[i,t] = sum_c a_src[t,c] M[i,tk+c] (kernels.hpp:385-423): a_src is h x k
           // row-major, so its flat index is the output column; k % 4 == 0 and
@@ -715,8 +770,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 8; ++j) {
             float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (bias && col0 + 4 * j < N) {
-              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0 + 4 * j));
+            if (bsh) {  // columns past N add lane 0's 0.f and are clipped by TMA
+              const float4 b = make_float4(__shfl_sync(0xffffffffu, bcur, 4 * j),
+                                           __shfl_sync(0xffffffffu, bcur, 4 * j + 1),
+                                           __shfl_sync(0xffffffffu, bcur, 4 * j + 2),
+                                           __shfl_sync(0xffffffffu, bcur, 4 * j + 3));
               v.x = __fadd_rn(v.x, b.x);
               v.y = __fadd_rn(v.y, b.y);
               v.z = __fadd_rn(v.z, b.z);
@@ -725,10 +783,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (EPI & 2) {
               mo[j] = (v.x > 0.f ? 1u : 0u) | (v.y > 0.f ? 1u : 0u) << 8 |
                       (v.z > 0.f ? 1u : 0u) << 16 | (v.w > 0.f ? 1u : 0u) << 24;
-              v.x = v.x > 0.f ? v.x : 0.f;
-              v.y = v.y > 0.f ? v.y : 0.f;
-              v.z = v.z > 0.f ? v.z : 0.f;
-              v.w = v.w > 0.f ? v.w : 0.f;
+              if constexpr ((EPI & 32) != 0) {  // ELU(1), as k_act_fwd
+                // exp for every element, then a select: a branch around each
+                // expf serialises the chunk (3x slower epilogue, measured)
+                const float ex = expf(v.x) - 1.f, ey = expf(v.y) - 1.f;
+                const float ez = expf(v.z) - 1.f, ew = expf(v.w) - 1.f;
+                v.x = v.x > 0.f ? v.x : ex;
+                v.y = v.y > 0.f ? v.y : ey;
+                v.z = v.z > 0.f ? v.z : ez;
+                v.w = v.w > 0.f ? v.w : ew;
+              } else {
+                v.x = v.x > 0.f ? v.x : 0.f;
+                v.y = v.y > 0.f ? v.y : 0.f;
+                v.z = v.z > 0.f ? v.z : 0.f;
+                v.w = v.w > 0.f ? v.w : 0.f;
+              }
             }
             if ((EPI & 4) && !(EPI & 16)) {
               const uint32_t w = (&mk[j >> 2].x)[j & 3];
@@ -748,7 +817,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
           }
           if ((EPI & 2) && mrow) {
-            uint4* mp = reinterpret_cast<uint4*>(sc.relu_out + (int64_t)row * N + col0);
+            uint4* mp = reinterpret_cast<uint4*>(sc.relu_out + (int64_t)row * sc.ldc + col0);
             mp[0] = make_uint4(mo[0], mo[1], mo[2], mo[3]);
             mp[1] = make_uint4(mo[4], mo[5], mo[6], mo[7]);
           }
@@ -783,9 +852,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                  : __uint_as_float(r[j]);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[abuf]);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -936,6 +1002,11 @@ static void dispatch(sgnn_ctx ctx, bool a_mn, bool b_mn, bool pre, const Maps& m
   if (sc.a_src) {
     if (b_mn) launch<false, true, BN, true, 9>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     else launch<false, false, BN, true, 9>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    return;
+  }
+  if (sc.relu_out && sc.elu) {
+    if (b_mn) launch<false, true, BN, true, 34>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
+    else launch<false, false, BN, true, 34>(ctx, mp, M, N, K, splits, kchunk, C, bias, part, tma_store, cs_part, sc);
     return;
   }
   if (sc.relu_out) {
@@ -1099,7 +1170,7 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
                              float* C, int32_t ldc, const float* bias, float* colsum_b,
                              const float* att_src, const float* att_dst, float* s_out,
                              float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
-                             const float* elu_saved);
+                             const float* elu_saved, bool elu_out = false);
 
 bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                  int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
@@ -1115,10 +1186,12 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
 // block of an n x (h k) slab.  false (nothing launched) if not supported.
 bool gemm_tc_f32_pitched(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
                          const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
-                         float* C, int32_t ldc, const float* bias) {
+                         float* C, int32_t ldc, const float* bias, float* colsum_b,
+                         uint8_t* elu_mask) {
   if ((lda & 3) || (ldb & 3) || (ldc & 3)) return false;
-  return gemm_tc_f32_impl(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias, nullptr,
-                          nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr);
+  return gemm_tc_f32_impl(ctx, A, ra, ca, lda, B, rb, cb, ldb, ta, tb, C, ldc, bias, colsum_b,
+                          nullptr, nullptr, nullptr, nullptr, 0, elu_mask, nullptr, nullptr,
+                          elu_mask != nullptr);
 }
 
 static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
@@ -1126,7 +1199,7 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
                              float* C, int32_t ldc, const float* bias, float* colsum_b,
                              const float* att_src, const float* att_dst, float* s_out,
                              float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
-                             const float* elu_saved) {
+                             const float* elu_saved, bool elu_out) {
   using namespace tc;
   if (tc_disabled()) return false;
   const int M = ta ? ca : ra, K = ta ? ra : ca, N = tb ? rb : cb;
@@ -1135,7 +1208,10 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
   // tiny: SIMT is fine (pitched operands have no SIMT path)
   if (!pitched && (int64_t)M * N * K < (int64_t)1 << 20) return false;
   if (ldc <= 0) ldc = N;
-  if (pitched && (colsum_b || att_src || relu_out || mask_in || elu_saved)) return false;
+  // pitched: output masks / column sums are fine, the fused scores and the
+  // activation backward read row-major n x N side arrays
+  if (pitched && (att_src || mask_in || elu_saved)) return false;
+  if (elu_out && !relu_out) return false;
   static const bool no_pad = getenv("SGNN_NO_PAD") != nullptr;  // dev switch
   if (!pitched && ((ca & 3) || (cb & 3))) {  // 16-byte row pitches for TMA: stage padded operands
     if (no_pad) return false;
@@ -1229,6 +1305,7 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
     sc.k = hk;
   }
   sc.relu_out = relu_out;
+  sc.elu = elu_out;
   sc.mask_in = mask_in;
   sc.elu_saved = elu_saved;
   sc.drain = drain;

@@ -144,9 +144,14 @@ void spmm_csr(sgnn_ctx ctx, int32_t n_rows, const int32_t* rowptr, const int32_t
 // multiples of 4 floats); false when the shape is not supported
 // false when SGNN_DISABLE_TCGEN05=1 (A/B switch of the tcgen05 GEMMs)
 bool gemm_tc_available();
+// colsum_b: fused column sums of B (MN-major B only, as gemm_tn_colsum);
+// elu_mask: ELU(1) applied to C (+ bias) with its byte mask written at the
+// same pitch as C (k_act_fwd's expressions; whole 32-column chunks).  false:
+// nothing was written, the caller runs the unfused pieces.
 bool gemm_tc_f32_pitched(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, int32_t lda,
                          const float* B, int32_t rb, int32_t cb, int32_t ldb, bool ta, bool tb,
-                         float* C, int32_t ldc, const float* bias);
+                         float* C, int32_t ldc, const float* bias, float* colsum_b = nullptr,
+                         uint8_t* elu_mask = nullptr);
 
 // row-padded staging copies of float32 matrices (gemm_tc.cu): zero-padded to
 // ocols columns / back to ocols columns with an optional bias add
