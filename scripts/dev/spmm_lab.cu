@@ -62,6 +62,39 @@ __global__ void __launch_bounds__(256, MINB) k_v0(int n, const int* __restrict__
   __stcs(C + (uint32_t)row * 32u + lane, acc);
 }
 
+// ---- V3: column windows -- window w = blockIdx.y (or a separate launch) of
+// 128 / W floats, 32 / W lanes per row, W rows per warp: the gathered table
+// per phase is 1/W of B, so it stays L2-resident while the window runs ------
+template <int W, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_win(int n, const int* __restrict__ rowptr,
+                                                    const int* __restrict__ cols,
+                                                    const float* __restrict__ vals,
+                                                    const float4* __restrict__ B,
+                                                    float4* __restrict__ C, int wfix) {
+  constexpr int L = 32 / W;
+  const int lane = threadIdx.x & 31, sub = lane / L, vec = lane % L;
+  const int row = (int)(((blockIdx.x * 256u + threadIdx.x) >> 5) * W + sub);
+  const int w = wfix >= 0 ? wfix : (int)blockIdx.y;
+  if (row >= n) return;
+  const int beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  const float4* Bw = B + w * L + vec;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int e = beg;
+  for (; e + U <= end; e += U) {
+    int c[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldg(cols + e + u), v[u] = __ldg(vals + e + u);
+    float4 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) b[u] = __ldg(Bw + (uint32_t)c[u] * 32u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc4(acc, v[u], b[u]);
+  }
+  for (; e < end; ++e) acc4(acc, __ldg(vals + e), __ldg(Bw + (uint32_t)__ldg(cols + e) * 32u));
+  __stcs(C + (uint32_t)row * 32u + w * L + vec, acc);
+}
+
 // ---- warp range by nnz: warp w of nw gets rows [r0, r1) -----------------------
 __device__ __forceinline__ int lower_row(const int* rowptr, int n, long long target) {
   // first row r with rowptr[r] >= target
@@ -336,6 +369,19 @@ int main(int argc, char** argv) {
   run("v0 U=2 minB=8", [&] { k_v0<2, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, true);
   run("v0 U=4 minB=6", [&] { k_v0<4, 6><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
   run("v0 U=1 minB=8", [&] { k_v0<1, 8><<<g0, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C); }, false);
+
+#define WIN(W, U, MINB)                                                                           \
+  {                                                                                               \
+    const dim3 gw((n + 8 * W - 1) / (8 * W), W);                                                  \
+    run("win W=" #W " U=" #U " grid.y", [&] { k_win<W, U, MINB><<<gw, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C, -1); }, false); \
+    run("win W=" #W " U=" #U " launches", [&] { for (int w = 0; w < W; ++w) k_win<W, U, MINB><<<gw.x, 256, 0, st>>>(n, d_rp, d_c, d_v, (float4*)d_B, (float4*)d_C, w); }, false); \
+  }
+  WIN(2, 2, 8)
+  WIN(2, 4, 6)
+  WIN(4, 2, 8)
+  WIN(4, 4, 6)
+  WIN(8, 4, 6)
+  if (argc > 1 && argv[1][0] == 'w') return 0;
 
 #define VR(S, G, TMA, WPB, CPS)                                                                \
   if (argc > 1) {                                                                                            \
