@@ -160,6 +160,20 @@ __device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8_async(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait8(uint32_t (&r)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -593,6 +607,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_of(t, z, m0, n0, kb, nk);
       int abuf = tl & 1;
       const int row = m0 + q * 32 + lane;
+      }
       // activation-backward inputs of this row's next 32 columns (mask bytes,
       // saved ELU outputs): fetched one chunk ahead -- the first while the
       // accumulator is still being produced -- so their latency overlaps the
@@ -628,13 +643,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&tfull[b], (dr / 3) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+            // two-deep pipeline: the 8-column load c + 8 is in flight while
+            // columns c are added (same adds, same order; 8-wide keeps the
+            // BN sums plus both buffers inside the register budget)
+            uint32_t ra[8], rb[8];
+            tmem_ld8_async(ta, ra);
 #pragma unroll
             for (int c = 0; c < BN; c += 16) {
-              uint32_t r[16];
-              tmem_ld16(ta + c, r);
+              tmem_wait8(ra);
+              tmem_ld8_async(ta + c + 8, rb);
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                sum[c + j] = __fadd_rn(sum[c + j], __uint_as_float(r[j]));
+              for (int j = 0; j < 8; ++j)
+                sum[c + j] = __fadd_rn(sum[c + j], __uint_as_float(ra[j]));
+              tmem_wait8(rb);
+              if (c + 16 < BN) tmem_ld8_async(ta + c + 16, ra);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                sum[c + 8 + j] = __fadd_rn(sum[c + 8 + j], __uint_as_float(rb[j]));
             }
             if (ks + 1 < nk) {
               asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
