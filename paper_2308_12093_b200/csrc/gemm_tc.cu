@@ -607,7 +607,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_of(t, z, m0, n0, kb, nk);
       int abuf = tl & 1;
       const int row = m0 + q * 32 + lane;
-      }
       // activation-backward inputs of this row's next 32 columns (mask bytes,
       // saved ELU outputs): fetched one chunk ahead -- the first while the
       // accumulator is still being produced -- so their latency overlaps the
