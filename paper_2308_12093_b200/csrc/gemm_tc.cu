@@ -277,6 +277,11 @@ struct EpiScores {
   // accumulations per k-block into one growing sum (5e-6 relative bias at
   // K = 500, measured); the final sum goes back to TMEM for the epilogue
   bool drain = false;
+  // k-blocks per drained partial (1, or 2 for unsplit GEMMs of moderate K:
+  // the drain's TMEM read -- 64 B/clk -- costs 8 BN cycles per partial
+  // against 6 BN cycles of MMAs per k-block, so draining every k-block made
+  // the K = 320 Gat2 d_input GEMM epilogue-bound)
+  int drain_group = 1;
   // row pitch of C in elements (0: N) -- column blocks of a wider matrix
   int ldc = 0;
 };
@@ -432,8 +437,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
+        const int dg = sc.drain_group;
         for (int ks = 0; ks < nk; ++ks, ++it) {
-          if (kdrain) {  // every k-block accumulates afresh into the next accumulator
+          const bool gfirst = ks % dg == 0, glast = ks % dg == dg - 1 || ks + 1 == nk;
+          if (kdrain && gfirst) {  // every k-block group accumulates afresh into the next accumulator
             abuf = dr % nacc;
             tacc = tmem + (uint32_t)(abuf * BN);
             mbar_wait(&tempty[abuf], ((dr / nacc) & 1) ^ 1);
@@ -452,15 +459,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
             const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
             const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
-            const uint32_t acc = ((ks > 0 && !kdrain) || kk > 0) ? 1u : 0u;
+            const uint32_t acc = ((ks > 0 && !kdrain) || (kdrain && !gfirst) || kk > 0) ? 1u : 0u;
             mma_tf32_ts(tacc, ta + kk * 8, dbh, idesc, acc);       // hi . hi
             mma_tf32_ts(tacc, ta + kk * 8, dbl, idesc, 1u);        // hi . lo
             mma_tf32_ts(tacc, ta + 32 + kk * 8, dbh, idesc, 1u);   // lo . hi
           }
           umma_commit(&empty[s]);   // smem stage free
           umma_commit(&aempty[a]);  // TMEM A buffer free
-          if (kdrain) {
-            umma_commit(&tfull[abuf]);  // this k-block's partial ready for the drain
+          if (kdrain && glast) {
+            umma_commit(&tfull[abuf]);  // this group's partial ready for the drain
             ++dr;
           }
         }
@@ -637,7 +644,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float sum[BN];
 #pragma unroll
           for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-          for (int ks = 0; ks < nk; ++ks, ++dr) {
+          const int ng = (nk + sc.drain_group - 1) / sc.drain_group;
+          for (int ks = 0; ks < ng; ++ks, ++dr) {
             const int b = dr % 3;
             mbar_wait(&tfull[b], (dr / 3) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -660,7 +668,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 8; ++j)
                 sum[c + 8 + j] = __fadd_rn(sum[c + 8 + j], __uint_as_float(rb[j]));
             }
-            if (ks + 1 < nk) {
+            if (ks + 1 < ng) {
               asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
               __syncwarp();
               if (lane == 0) mbar_arrive(&tempty[b]);
@@ -1333,6 +1341,15 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
   sc.mask_in = mask_in;
   sc.elu_saved = elu_saved;
   sc.drain = drain;
+  {
+    static const int kGroupMax = [] {  // dev knob SGNN_DRAIN_GROUP (default 2)
+      const char* e = getenv("SGNN_DRAIN_GROUP");
+      return e ? std::max(1, atoi(e)) : 2;
+    }();
+    // split-K partials (dTheta over K = n: long, cancelling sums) keep
+    // one k-block per partial; unsplit GEMMs up to K = 2048 group
+    sc.drain_group = (drain && splits == 1 && K <= 2048) ? kGroupMax : 1;
+  }
   if (elu_saved && (!mask_in || (reinterpret_cast<uintptr_t>(elu_saved) & 15))) return false;
   if ((sc.a_src || relu_out || mask_in) && (a_mn || !pre)) return false;
   // TMA-store epilogue for the final output (row pitch N*4 must be 16 B aligned)

@@ -158,9 +158,14 @@ def gat_case(d, ref, orc, shape, h, k, m, levels):
     results = {}
     for level in levels:
         out, cache = d.gat_forward(P, X, th, a_s, a_d, b, h, 0.2, level)
-        if dev_mask is None:
-            _, mk = cache.edge_values(P, th, a_s, a_d)
-            dev_mask = mk.t().cpu().numpy().astype(bool)  # edge-major q x h
+        # the decisions of THIS level's backward: levels recompute the scores
+        # by different routes (the fused GEMM epilogue at none, node_scores
+        # from the cached M at features), whose roundings may put a |y| ~ 0
+        # edge on different sides
+        _, mk = cache.edge_values(P, th, a_s, a_d)
+        mask = mk.t().cpu().numpy().astype(bool)  # edge-major q x h
+        if dev_mask is None or not np.array_equal(mask, dev_mask):
+            dev_mask = mask
             flips, far = gat_f64.ill_conditioned_flips(st["y"], dev_mask)
             assert far == 0, f"{far} of {flips} LeakyReLU decisions differ at |y| >= 1e-5 scale"
             want_g = gat_f64.backward(rp, cl, h64(G), args[0], args[1], args[2], args[3], h,
