@@ -185,6 +185,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -385,7 +393,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tmem_a = tmem + CF::NACC * BN;  // A buffers after the accumulators
 
   if (warp == 0) {
@@ -423,55 +431,77 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // the whole warp walks the loop, so the MMA operands are warp-uniform
+    // values the compiler keeps in uniform registers (issued from one lane
+    // inside the loop it wrapped every tcgen05.mma in an ELECT / R2UR
+    // uniformization loop: 8 instructions per MMA; X.Theta 72 -> 66 us,
+    // G.Theta^T 68 -> 60 us measured); one elected lane issues MMAs / commits
+    {
+      const bool leader = elect_one();
       constexpr uint32_t idesc = instr_desc(BN, false, B_MN);  // A from TMEM is K-major
       int it = 0, tl = 0, dr = 0;
-      const bool kdrain = sc.drain;  // per-k-block accumulators (three)
+      const bool kdrain = sc.drain;  // per-k-block(-group) accumulators (three)
       const int nacc = 3;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
-        int z, m0, n0, kb, nk;
-        tile_of(t, z, m0, n0, kb, nk);
-        int abuf = tl & 1;
-        uint32_t tacc = tmem + (uint32_t)(abuf * BN);
-        if (!kdrain) {
-          mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        }
-        const int dg = sc.drain_group;
-        for (int ks = 0; ks < nk; ++ks, ++it) {
-          const bool gfirst = ks % dg == 0, glast = ks % dg == dg - 1 || ks + 1 == nk;
-          if (kdrain && gfirst) {  // every k-block group accumulates afresh into the next accumulator
-            abuf = dr % nacc;
-            tacc = tmem + (uint32_t)(abuf * BN);
-            mbar_wait(&tempty[abuf], ((dr / nacc) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          }
-          const int s = it % S, a = it % NA;
-          mbar_wait(&afull[a], (it / NA) & 1);  // implies full[s] (converters waited on it)
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ta = tmem_a + (uint32_t)(a * 64);
-          const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+      // one k-block into accumulator tacc (fresh: its first MMA overwrites)
+      auto kblock = [&](uint32_t tacc, bool fresh) {
+        const int s = it % S, a = it % NA;
+        mbar_wait(&afull[a], (it / NA) & 1);  // implies full[s] (converters waited on it)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem_a + (uint32_t)(a * 64);
+        const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            // B K-major (SW128): +32 B inside the swizzled row, SBO 1024.
-            // B MN-major (SW128_BASE32B): +1024 B per 8 K-rows, LBO 4096, SBO 512.
-            const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
-            const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
-            const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
-            const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
-            const uint32_t acc = ((ks > 0 && !kdrain) || (kdrain && !gfirst) || kk > 0) ? 1u : 0u;
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          // B K-major (SW128): +32 B inside the swizzled row, SBO 1024.
+          // B MN-major (SW128_BASE32B): +1024 B per 8 K-rows, LBO 4096, SBO 512.
+          const uint32_t boff = B_MN ? kk * 1024 : kk * 32;
+          const uint32_t blb = B_MN ? 4096 : 16, bsb = B_MN ? 512 : 1024, blt = B_MN ? 1 : 2;
+          const uint64_t dbh = smem_desc(bh + boff, blb, bsb, blt);
+          const uint64_t dbl = smem_desc(bl + boff, blb, bsb, blt);
+          const uint32_t acc = (!fresh || kk > 0) ? 1u : 0u;
+          if (leader) {
             mma_tf32_ts(tacc, ta + kk * 8, dbh, idesc, acc);       // hi . hi
             mma_tf32_ts(tacc, ta + kk * 8, dbl, idesc, 1u);        // hi . lo
             mma_tf32_ts(tacc, ta + 32 + kk * 8, dbh, idesc, 1u);   // lo . hi
           }
+        }
+        if (leader) {
           umma_commit(&empty[s]);   // smem stage free
           umma_commit(&aempty[a]);  // TMEM A buffer free
-          if (kdrain && glast) {
-            umma_commit(&tfull[abuf]);  // this group's partial ready for the drain
-            ++dr;
+        }
+        __syncwarp();
+        ++it;
+      };
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        int z, m0, n0, kb, nk;
+        tile_of(t, z, m0, n0, kb, nk);
+        if (!kdrain) {  // the tile's accumulator: one of two, by tile parity
+          const int abuf = tl & 1;
+          const uint32_t tacc = tmem + (uint32_t)(abuf * BN);
+          mbar_wait(&tempty[abuf], ((tl >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int ks = 0; ks < nk; ++ks) kblock(tacc, ks == 0);
+          if (leader) umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
+          __syncwarp();
+        } else {  // every group of 1-2 k-blocks into the next of three accumulators
+          const int gm = sc.drain_group - 1;
+          uint32_t tacc = 0;
+          int abuf = 0;
+          for (int ks = 0; ks < nk; ++ks) {
+            const bool gfirst = (ks & gm) == 0, glast = (ks & gm) == gm || ks + 1 == nk;
+            if (gfirst) {
+              abuf = dr % nacc;
+              tacc = tmem + (uint32_t)(abuf * BN);
+              mbar_wait(&tempty[abuf], ((dr / nacc) & 1) ^ 1);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            kblock(tacc, gfirst);
+            if (glast) {
+              if (leader) umma_commit(&tfull[abuf]);  // this group's partial ready for the drain
+              __syncwarp();
+              ++dr;
+            }
           }
         }
-        if (!kdrain) umma_commit(&tfull[abuf]);  // accumulator ready for the epilogue
       }
     }
   } else if (warp < 6) {
@@ -644,7 +674,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float sum[BN];
 #pragma unroll
           for (int j = 0; j < BN; ++j) sum[j] = 0.f;
-          const int ng = (nk + sc.drain_group - 1) / sc.drain_group;
+          const int ng = sc.drain_group == 1 ? nk : (nk + 1) >> 1;
           for (int ks = 0; ks < ng; ++ks, ++dr) {
             const int b = dr % 3;
             mbar_wait(&tfull[b], (dr / 3) & 1);
@@ -701,9 +731,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // is processed, and the accumulator goes back to the MMA warp as soon as
       // its last chunk is in registers
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * BN);
-      const float* bsh = (tma_store && !part) ? bias : nullptr;  // bias by shuffle
-      // (not with the ELU backward's saved-value prefetch: registers would spill)
-      constexpr bool PIPE = (EPI & 16) == 0;
+      // Only the ELU forward epilogue (exp per element) gains from it:
+      // measured, the plain / bias / ReLU epilogues are 4 us slower with it
+      // (X.Theta 80 -> 84 us), the ELU one 131 -> 96 us faster
+      constexpr bool PIPE = (EPI & 32) != 0;
+      const float* bsh = (PIPE && tma_store && !part) ? bias : nullptr;  // bias by shuffle
       uint32_t rn[32];
       if constexpr (PIPE) tmem_ld32_async(tacc, rn);
       float bnx = (bsh && n0 + lane < N) ? __ldg(bsh + n0 + lane) : 0.f;
@@ -802,6 +834,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 8; ++j) {
             float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            if (!bsh && bias && col0 + 4 * j < N) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + col0 + 4 * j));
+              v.x = __fadd_rn(v.x, b.x);
+              v.y = __fadd_rn(v.y, b.y);
+              v.z = __fadd_rn(v.z, b.z);
+              v.w = __fadd_rn(v.w, b.w);
+            }
             if (bsh) {  // columns past N add lane 0's 0.f and are clipped by TMA
               const float4 b = make_float4(__shfl_sync(0xffffffffu, bcur, 4 * j),
                                            __shfl_sync(0xffffffffu, bcur, 4 * j + 1),
@@ -1344,7 +1383,7 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
   {
     static const int kGroupMax = [] {  // dev knob SGNN_DRAIN_GROUP (default 2)
       const char* e = getenv("SGNN_DRAIN_GROUP");
-      return e ? std::max(1, atoi(e)) : 2;
+      return (e && atoi(e) <= 1) ? 1 : 2;
     }();
     // split-K partials (dTheta over K = n: long, cancelling sums) keep
     // one k-block per partial; unsplit GEMMs up to K = 2048 group
