@@ -216,6 +216,27 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
+// explicit shared-space accesses (the 1024-aligned smem base is computed
+// through an integer, so plain dereferences compile to generic LD / ST)
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f32x4(uint32_t a, const float4& v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
 // Split a raw fp32 smem tile in place into hi (tf32-exact) and write lo.
@@ -582,13 +603,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int p = r & 31, c32 = p >> 3, e = p & 7;
 #pragma unroll
           for (int kr = 0; kr < 32; ++kr)
-            v[kr] = *reinterpret_cast<const float*>(bx + kr * 128 + ((c32 ^ (kr & 3)) << 5) + e * 4);
+            v[kr] = lds_f32(smem_u32(bx) + kr * 128 + ((c32 ^ (kr & 3)) << 5) + e * 4);
         } else {
           // row r: 128 B, 16 B chunks swizzled with (row % 8)
           const uint8_t* row = base + r * 128;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 x = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+            const float4 x = lds_f32x4(smem_u32(row) + ((c ^ (r & 7)) << 4));
             v[4 * c] = x.x;
             v[4 * c + 1] = x.y;
             v[4 * c + 2] = x.z;
@@ -885,7 +906,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z = (w & 0xff0000u) ? v.z : __fmul_rn(__fadd_rn(e.z, 1.f), v.z);
               v.w = (w & 0xff000000u) ? v.w : __fmul_rn(__fadd_rn(e.w, 1.f), v.w);
             }
-            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+            sts_f32x4(smem_u32(buf) + lane * 128 + ((j ^ (lane & 7)) << 4), v);
           }
           if ((EPI & 2) && mrow) {
             uint4* mp = reinterpret_cast<uint4*>(sc.relu_out + (int64_t)row * sc.ldc + col0);
