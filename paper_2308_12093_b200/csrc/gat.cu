@@ -1066,6 +1066,16 @@ static void gat_backward_reordered(sgnn_ctx ctx, sgnn_pattern p, const float* G,
   launched(ctx);
 }
 
+// SGNN_GAT_FUSE=0: the forward runs attention and aggregation as two
+// kernels (A/B switch; the results are bit-identical either way)
+static bool gat_fuse_on() {
+  static const bool on = [] {
+    const char* e = getenv("SGNN_GAT_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class T>
 void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T* theta,
                    const T* a_src, const T* a_dst, const T* bias, int32_t h, int32_t k,
@@ -1123,21 +1133,34 @@ void gat_forward_t(sgnn_ctx ctx, sgnn_pattern p, const T* X, int32_t m, const T*
     }
     const LongRows& pr = long_rows(ctx, p->long_rows, n, rp);
     g2::SegArgs sk = skip_long(pr);
-    HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
-                         n, rp, ci, sp, dp, (float)beta, ap, mp, sk.longest)));
-    launched(ctx);
-    if (pr.nlong) {  // hub rows: a block per row
-      HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
-                          pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta, ap, mp)));
-      launched(ctx);
-    }
     if (elu_mask && pr.nlong == 0) {  // ELU in the aggregation epilogue (no hub combine)
       sk.elu_mask = elu_mask;
       if (elu_fused) *elu_fused = true;
     }
-    HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(n, rp, ci, ap, M4, k,
-                                                                        b4, o4, sk)));
-    launched(ctx);
+    if (v2_windows<T>(h, k) == 1 && gat_fuse_on()) {
+      // attention + aggregation of the hub-free rows in one kernel
+      // (bit-identical to k_gat_attn4 + k_gat_agg2; SGNN_GAT_FUSE=0 splits them)
+      HR_SWITCH(h, R2, (g2::k_gat_attnagg<HH, RR><<<(unsigned)ceil_div(n, 16), 256, 0, st>>>(
+                           n, rp, ci, sp, dp, (float)beta, ap, mp, M4, k, b4, o4, sk)));
+      launched(ctx);
+      if (pr.nlong) {  // hub rows: a block per row
+        HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
+                            pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta, ap, mp)));
+        launched(ctx);
+      }
+    } else {
+      HR_SWITCH(h, R2, (g2::k_gat_attn4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
+                           n, rp, ci, sp, dp, (float)beta, ap, mp, sk.longest)));
+      launched(ctx);
+      if (pr.nlong) {  // hub rows: a block per row
+        HR_SWITCH(h, 1, (g2::k_gat_attn_long<HH><<<pr.nlong, 256, 0, st>>>(
+                            pr.long_row.as<int32_t>(), rp, ci, sp, dp, (float)beta, ap, mp)));
+        launched(ctx);
+      }
+      HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR><<<dim3(v2_grid(n), v2_windows<T>(h, k)), 256, 0, st>>>(n, rp, ci, ap, M4, k,
+                                                                          b4, o4, sk)));
+      launched(ctx);
+    }
     if (pr.nlong) {  // hub rows: segment partials, combined in order (+ bias)
       DevBuf part((size_t)pr.nseg * hk * sizeof(float), st);
       HR_SWITCH(h, R2, (g2::k_gat_agg2<HH, RR, true><<<dim3(v2_grid(pr.nseg), v2_windows<T>(h, k)), 256, 0, st>>>(

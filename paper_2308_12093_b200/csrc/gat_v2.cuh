@@ -357,15 +357,24 @@ __device__ __forceinline__ uint32_t restage_alpha(int32_t ee, const int32_t* __r
 // attention load per lane (its head; 32-byte sector per edge) and R 16-byte
 // row vectors, U edges in flight; <= 40 registers for 48 resident warps/SM.
 // ---------------------------------------------------------------------------
-template <int H, int R, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
-    k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-               const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
-               const float4* __restrict__ bias, float4* __restrict__ out, SegArgs sg = {}) {
+// LDA: the attention load (__ldg; __ldcg when the same kernel just wrote it)
+struct LdgA {
+  static __device__ __forceinline__ float ld(const float* p) { return __ldg(p); }
+};
+struct LdcgA {
+  static __device__ __forceinline__ float ld(const float* p) { return __ldcg(p); }
+};
+
+template <int H, int R, bool SEG, class LDA>
+__device__ __forceinline__ void agg2_row(int32_t i, int vo, int32_t n,
+                                         const int32_t* __restrict__ rowptr,
+                                         const int32_t* __restrict__ cols,
+                                         const float* __restrict__ alpha,
+                                         const float4* __restrict__ M, int32_t k,
+                                         const float4* __restrict__ bias,
+                                         float4* __restrict__ out, const SegArgs& sg) {
   constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
   const int lane = threadIdx.x & 31;
-  const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
-  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
   int32_t beg, end;
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
       c[u] = (uint32_t)__ldg(cols + e + u);
 #pragma unroll
       for (int r = 0; r < R; ++r)  // once per head when heads span whole chunks
-        a[u][r] = r % C == 0 ? __ldg(alpha + (int64_t)(e + u) * H + tr[r]) : a[u][r - 1];
+        a[u][r] = r % C == 0 ? LDA::ld(alpha + (int64_t)(e + u) * H + tr[r]) : a[u][r - 1];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
     for (int r = 0; r < R; ++r) {
       const uint32_t v = vo + r * 32 + lane;
       if (v < (uint32_t)fv)
-        fma4(acc[r], __ldg(alpha + (int64_t)e * H + tr[r]), __ldg(M + c * (uint32_t)fv + v));
+        fma4(acc[r], LDA::ld(alpha + (int64_t)e * H + tr[r]), __ldg(M + c * (uint32_t)fv + v));
     }
   }
 #pragma unroll
@@ -447,6 +456,16 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
       __stcs(out + (int64_t)i * fv + v, o);
     }
   }
+}
+
+template <int H, int R, bool SEG = false>
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
+    k_gat_agg2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+               const float* __restrict__ alpha, const float4* __restrict__ M, int32_t k,
+               const float4* __restrict__ bias, float4* __restrict__ out, SegArgs sg = {}) {
+  // column window blockIdx.y (slabs wider than 32R vectors), one warp per row
+  agg2_row<H, R, SEG, LdgA>((int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5),
+                            blockIdx.y * 32 * R, n, rowptr, cols, alpha, M, k, bias, out, sg);
 }
 
 // ---------------------------------------------------------------------------
@@ -1062,16 +1081,15 @@ __device__ __forceinline__ void group_allreduce(float (&v)[H], int gl, Op op) {
 }
 
 template <int H>
-__global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __restrict__ rowptr,
-                                                   const int32_t* __restrict__ cols,
-                                                   const float* __restrict__ s,
-                                                   const float* __restrict__ d, float beta,
-                                                   float* __restrict__ alpha,
-                                                   uint8_t* __restrict__ mask,
-                                                   int32_t longest = 0x7fffffff,
-                                                   float* __restrict__ stats = nullptr) {
+__device__ __forceinline__ void attn4_rows(int32_t i, int32_t n, const int32_t* __restrict__ rowptr,
+                                           const int32_t* __restrict__ cols,
+                                           const float* __restrict__ s,
+                                           const float* __restrict__ d, float beta,
+                                           float* __restrict__ alpha,
+                                           uint8_t* __restrict__ mask, int32_t longest,
+                                           float* __restrict__ stats) {
+  // i: this 16-lane group's row (two rows per warp)
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
-  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
   if (i < n) {
     beg = __ldg(rowptr + i);
@@ -1152,6 +1170,45 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
       if (mask) st_mask<H>(mask + (int64_t)e * H, pos);
     }
   }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const int32_t* __restrict__ cols,
+                                                   const float* __restrict__ s,
+                                                   const float* __restrict__ d, float beta,
+                                                   float* __restrict__ alpha,
+                                                   uint8_t* __restrict__ mask,
+                                                   int32_t longest = 0x7fffffff,
+                                                   float* __restrict__ stats = nullptr) {
+  attn4_rows<H>((int32_t)((blockIdx.x * 256u + threadIdx.x) / GS), n, rowptr, cols, s, d, beta,
+                alpha, mask, longest, stats);
+}
+
+// ---------------------------------------------------------------------------
+// Attention + aggregation in one kernel (one column window, hub-free rows):
+// a warp computes the attention of its two rows exactly as k_gat_attn4 (16
+// lanes per row; alpha / mask written edge-major, the cache at level full)
+// and then aggregates each of the two rows as k_gat_agg2 (the whole warp per
+// row), reading the attention back through L2 (__ldcg: written by this warp,
+// ordered by __syncwarp) -- bit-identical to the two-kernel path, one launch
+// and one alpha round trip to HBM fewer, and the latency-bound softmax phase
+// overlaps other warps' gathers.
+// ---------------------------------------------------------------------------
+template <int H, int R>
+__global__ void __launch_bounds__(256, R <= 2 ? 4 : (R <= 4 ? 3 : 2))
+    k_gat_attnagg(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                  const float* __restrict__ s, const float* __restrict__ d, float beta,
+                  float* __restrict__ alpha, uint8_t* __restrict__ mask,
+                  const float4* __restrict__ M, int32_t k, const float4* __restrict__ bias,
+                  float4* __restrict__ out, SegArgs sg) {
+  const int32_t w = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  attn4_rows<H>(2 * w + (lane >= GS ? 1 : 0), n, rowptr, cols, s, d, beta, alpha, mask,
+                sg.longest, nullptr);
+  __syncwarp();
+  agg2_row<H, R, false, LdcgA>(2 * w, 0, n, rowptr, cols, alpha, M, k, bias, out, sg);
+  agg2_row<H, R, false, LdcgA>(2 * w + 1, 0, n, rowptr, cols, alpha, M, k, bias, out, sg);
 }
 
 template <int H>

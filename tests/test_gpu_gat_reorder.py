@@ -143,3 +143,44 @@ np.save(sys.argv[2], np.concatenate([[float(loss)], out.double().cpu().numpy().r
             a, b = res
             rel = np.abs(a - b).max() / np.abs(b).max()
             assert rel < 1e-4, (level, rel)
+
+
+def test_fused_attention_aggregation_bit_identical():
+    """The forward's fused attention + aggregation kernel (k_gat_attnagg) gives
+    the same bits as k_gat_attn4 + k_gat_agg2 (SGNN_GAT_FUSE=0, child process)
+    for outputs, cached attention and the backward, on a uniform graph and on a
+    power-law graph with hub rows (those keep the segment path)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, '.')
+from paper_2308_12093_b200 import device as d
+res = []
+for kind, h, k in (("er", 8, 32), ("er", 4, 40), ("er", 2, 64), ("pl", 8, 8)):
+    n = 3000
+    s, t = d.synthetic_graph(n, 9.0, 3) if kind == "er" else d.powerlaw_graph(n, 12.0, 2.1, 5)
+    P = d.Pattern.gat_pattern(n, s, t)
+    X = d.random_uniform(n, 48, 4)
+    th, a_s, a_d, b = d.gat_params(48, h, k, 6)
+    G = d.random_uniform(n, h * k, 7)
+    for level in ("none", "full"):
+        out, c = d.gat_forward(P, X, th, a_s, a_d, b, h, 0.2, level)
+        al, mk = c.edge_values(P, th, a_s, a_d)
+        g = d.gat_backward(P, G, th, a_s, a_d, c, True)
+        res += [out.cpu().numpy().ravel(), al.cpu().numpy().ravel(), mk.cpu().numpy().ravel()]
+        res += [x.cpu().numpy().ravel() for x in g]
+np.save(sys.argv[1], np.concatenate([r.astype(np.float64) for r in res]))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as tmp:
+        out = []
+        for flag in ("1", "0"):
+            f = os.path.join(tmp, f"{flag}.npy")
+            subprocess.run([sys.executable, "-c", code, f], cwd=root,
+                           env=dict(os.environ, SGNN_GAT_FUSE=flag), check=True, timeout=300)
+            out.append(np.load(f))
+        assert np.array_equal(out[0], out[1])
