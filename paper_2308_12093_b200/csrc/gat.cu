@@ -781,6 +781,26 @@ static void sddmm2_launch(int mode, dim3 grid, cudaStream_t st, int32_t n, const
 #undef SDDMM2_GO
 }
 
+template <int HH, int RR>
+static void sddmm_sbwd_launch(int mode, cudaStream_t st, int32_t n, const int32_t* rp,
+                              const int32_t* ci, const float4* M4, const float4* G4, int32_t k,
+                              const float* al, const uint8_t* mk, double beta, float* da,
+                              float* dy, float* dS, const g2::SegArgs& sa) {
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(n, 16));  // two rows per warp
+#define SDSB_GO(PM) \
+  g2::k_gat_sddmm_sbwd<HH, RR, PM><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, al, mk, \
+                                                         (float)beta, da, dy, dS, sa)
+  switch (mode) {
+    case 1: SDSB_GO(1); return;
+    case 2: if constexpr (RR % 2 == 0) { SDSB_GO(2); return; } break;
+    case 4: if constexpr (RR % 4 == 0) { SDSB_GO(4); return; } break;
+    case 8: if constexpr (RR % 8 == 0) { SDSB_GO(8); return; } break;
+    default: break;
+  }
+#undef SDSB_GO
+  throw invalid_argument("gat: no fused SDDMM kernel for this head width");
+}
+
 // hub rows / columns of a pattern (LongRows plan): segment arguments
 static g2::SegArgs seg_args(const LongRows& pl, float* part = nullptr, float* ddpart = nullptr) {
   g2::SegArgs a;
@@ -1344,16 +1364,28 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const int L = k / 4;
     const unsigned wn = v2_windows<T>(h, k);
     const int smode = sddmm_mode(L, R2);
-    HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, false>(smode, dim3(v2_grid(n), wn), st, n, rp, ci, M4,
-                                                   G4, k, da.as<float>(), sk)));
+    // SDDMM + softmax backward of the hub-free rows in one kernel when the
+    // head dots reduce in registers (bit-identical to k_gat_sddmm2 +
+    // k_gat_sbwd4; SGNN_GAT_FUSE=0 splits them)
+    const bool fuse = wn == 1 && smode >= 1 && gat_fuse_on();
+    if (fuse) {
+      HR_SWITCH(h, R2, (sddmm_sbwd_launch<HH, RR>(smode, st, n, rp, ci, M4, G4, k, al, mk, beta,
+                                                  da.as<float>(), dy.as<float>(), dS.as<float>(),
+                                                  sk)));
+    } else {
+      HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, false>(smode, dim3(v2_grid(n), wn), st, n, rp, ci,
+                                                     M4, G4, k, da.as<float>(), sk)));
+    }
     if (pr.nlong)  // hub rows: per-edge outputs, segments write them directly
       HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, true>(smode, dim3(v2_grid(pr.nseg), wn), st, pr.nseg,
                                                     rp, ci, M4, G4, k, da.as<float>(), seg_args(pr))));
     launched(ctx);
-    HR_SWITCH(h, R2, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
-                         n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
-                         dS.as<float>(), sk.longest)));
-    launched(ctx);
+    if (!fuse) {
+      HR_SWITCH(h, R2, (g2::k_gat_sbwd4<HH><<<g2::sub_grid(n), 256, 0, st>>>(
+                           n, rp, al, mk, da.as<float>(), (float)beta, dy.as<float>(),
+                           dS.as<float>(), sk.longest)));
+      launched(ctx);
+    }
     if (pr.nlong) {
       HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pr.nlong, 256, 0, st>>>(
                           pr.long_row.as<int32_t>(), rp, al, mk, da.as<float>(), (float)beta,

@@ -100,23 +100,27 @@ __device__ __forceinline__ void allreduce(float (&v)[H], int lane, Op op) {
   }
 }
 
-template <int H>
+// CG: load through L2 (__ldcg) -- values this kernel wrote earlier (the
+// read-only __ldg path is not coherent with them)
+template <int H, bool CG = false>
 __device__ __forceinline__ void ld_heads(const float* __restrict__ p, float (&v)[H]) {
   if constexpr (H % 4 == 0) {
 #pragma unroll
     for (int q = 0; q < H / 4; ++q) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(p) + q);
+      const float4 x = CG ? __ldcg(reinterpret_cast<const float4*>(p) + q)
+                          : __ldg(reinterpret_cast<const float4*>(p) + q);
       v[4 * q] = x.x;
       v[4 * q + 1] = x.y;
       v[4 * q + 2] = x.z;
       v[4 * q + 3] = x.w;
     }
   } else if constexpr (H == 2) {
-    const float2 x = __ldg(reinterpret_cast<const float2*>(p));
+    const float2 x = CG ? __ldcg(reinterpret_cast<const float2*>(p))
+                        : __ldg(reinterpret_cast<const float2*>(p));
     v[0] = x.x;
     v[1] = x.y;
   } else {
-    v[0] = __ldg(p);
+    v[0] = CG ? __ldcg(p) : __ldg(p);
   }
 }
 
@@ -479,16 +483,23 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
 // per-vector partial dots go through shared memory and H*U lanes fold the
 // k/4 partials of their (edge, head).
 // ---------------------------------------------------------------------------
-template <int H, int R, int P2, bool SEG = false>
-__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
-    k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-                 const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
-                 float* __restrict__ da, SegArgs sg = {}) {
-  constexpr int U = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
-  __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : U][P2 ? 1 : 32 * R];  // P2 == 0 only
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int vo = blockIdx.y * 32 * R;  // column window (slabs wider than 32R vectors)
-  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+template <int R>
+struct SddmmU {
+  static constexpr int v = R >= 4 ? 1 : (R <= 2 ? GAT_U2 : 2);
+};
+
+// one row (or hub segment) i of the SDDMM over column window vo; sh_p: the
+// warp's shared-memory fold buffer (P2 == 0 only)
+template <int H, int R, int P2, bool SEG>
+__device__ __forceinline__ void sddmm2_row(int32_t i, int vo, int32_t n,
+                                           const int32_t* __restrict__ rowptr,
+                                           const int32_t* __restrict__ cols,
+                                           const float4* __restrict__ M,
+                                           const float4* __restrict__ G, int32_t k,
+                                           float* __restrict__ da, const SegArgs& sg,
+                                           float (*sh_p)[P2 ? 1 : 32 * R]) {
+  constexpr int U = SddmmU<R>::v;
+  const int lane = threadIdx.x & 31;
   if (i >= n) return;
   const int fv = H * k / 4, L = k / 4;
   int32_t beg, end, grow = i;  // grow: the row of dX' this warp dots against
@@ -617,7 +628,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (vo + r * 32 + lane < fv) sh_p[wib][u][r * 32 + lane] = p[r];
+          if (vo + r * 32 + lane < fv) sh_p[u][r * 32 + lane] = p[r];
       }
     }
     if constexpr (P2 == 0) {
@@ -626,12 +637,25 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
       if (lane < U * hw) {
         const int u = lane / hw, tl = lane % hw, t = vo / L + tl;
         float acc = 0.f;
-        for (int q = 0; q < L; ++q) acc += sh_p[wib][u][tl * L + q];
+        for (int q = 0; q < L; ++q) acc += sh_p[u][tl * L + q];
         if (e + u < end && t < H) da[(int64_t)(e + u) * H + t] = acc;
       }
       __syncwarp();
     }
   }
+}
+
+template <int H, int R, int P2, bool SEG = false>
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3))
+    k_gat_sddmm2(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                 const float4* __restrict__ M, const float4* __restrict__ G, int32_t k,
+                 float* __restrict__ da, SegArgs sg = {}) {
+  __shared__ float sh_p[P2 ? 1 : WPB][P2 ? 1 : SddmmU<R>::v][P2 ? 1 : 32 * R];  // P2 == 0 only
+  const int wib = threadIdx.x >> 5;
+  // column window blockIdx.y (slabs wider than 32R vectors), one warp per row
+  sddmm2_row<H, R, P2, SEG>((int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5),
+                            blockIdx.y * 32 * R, n, rowptr, cols, M, G, k, da, sg,
+                            sh_p[P2 ? 0 : wib]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1195,8 +1219,11 @@ __global__ void __launch_bounds__(256) k_gat_attn4(int32_t n, const int32_t* __r
 // and one alpha round trip to HBM fewer, and the latency-bound softmax phase
 // overlaps other warps' gathers.
 // ---------------------------------------------------------------------------
+#ifndef GAT_AA_MINB
+#define GAT_AA_MINB 5  // resident blocks per SM at R <= 2 (4: no spills, 10 us slower at Arxiv 8x32; 6 slower again)
+#endif
 template <int H, int R>
-__global__ void __launch_bounds__(256, R <= 2 ? 4 : (R <= 4 ? 3 : 2))
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_AA_MINB : (R <= 4 ? 3 : 2))
     k_gat_attnagg(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                   const float* __restrict__ s, const float* __restrict__ d, float beta,
                   float* __restrict__ alpha, uint8_t* __restrict__ mask,
@@ -1211,17 +1238,17 @@ __global__ void __launch_bounds__(256, R <= 2 ? 4 : (R <= 4 ? 3 : 2))
   agg2_row<H, R, false, LdcgA>(2 * w + 1, 0, n, rowptr, cols, alpha, M, k, bias, out, sg);
 }
 
-template <int H>
-__global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __restrict__ rowptr,
-                                                   const float* __restrict__ alpha,
-                                                   const uint8_t* __restrict__ mask,
-                                                   const float* __restrict__ da, float beta,
-                                                   float* __restrict__ dy,
-                                                   float* __restrict__ dS,
-                                                   int32_t longest = 0x7fffffff,
-                                                   float* __restrict__ stats = nullptr) {
+// softmax / LeakyReLU backward of row i (16 lanes per row); CG: dAlpha was
+// written by the same kernel (read through L2)
+template <int H, bool CG>
+__device__ __forceinline__ void sbwd4_rows(int32_t i, int32_t n,
+                                           const int32_t* __restrict__ rowptr,
+                                           const float* __restrict__ alpha,
+                                           const uint8_t* __restrict__ mask,
+                                           const float* __restrict__ da, float beta,
+                                           float* __restrict__ dy, float* __restrict__ dS,
+                                           int32_t longest, float* __restrict__ stats) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
-  const int32_t i = (int32_t)((blockIdx.x * 256u + threadIdx.x) / GS);
   int32_t beg = 0, end = 0;
   if (i < n) {
     beg = __ldg(rowptr + i);
@@ -1246,7 +1273,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     const int32_t e = beg + off + gl;
     if (off + gl < deg) {
       ld_heads<H>(alpha + (int64_t)e * H, a);
-      ld_heads<H>(da + (int64_t)e * H, g);
+      ld_heads<H, CG>(da + (int64_t)e * H, g);
 #pragma unroll
       for (int t = 0; t < H; ++t) dot[t] = fmaf(a[t], g[t], dot[t]);
     }
@@ -1259,7 +1286,7 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
     if (off + gl < deg) {
       if (!one) {
         ld_heads<H>(alpha + (int64_t)e * H, a);
-        ld_heads<H>(da + (int64_t)e * H, g);
+        ld_heads<H, CG>(da + (int64_t)e * H, g);
       }
       const uint32_t pos = ld_mask<H>(mask + (int64_t)e * H);
       float y[H];
@@ -1274,6 +1301,49 @@ __global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __r
   }
   group_allreduce<H>(rs, gl, OpSum());
   if (i < n && gl == 0 && !hub) st_heads<H>(dS + (int64_t)i * H, rs);
+}
+
+
+template <int H>
+__global__ void __launch_bounds__(256) k_gat_sbwd4(int32_t n, const int32_t* __restrict__ rowptr,
+                                                   const float* __restrict__ alpha,
+                                                   const uint8_t* __restrict__ mask,
+                                                   const float* __restrict__ da, float beta,
+                                                   float* __restrict__ dy,
+                                                   float* __restrict__ dS,
+                                                   int32_t longest = 0x7fffffff,
+                                                   float* __restrict__ stats = nullptr) {
+  sbwd4_rows<H, false>((int32_t)((blockIdx.x * 256u + threadIdx.x) / GS), n, rowptr, alpha, mask,
+                       da, beta, dy, dS, longest, stats);
+}
+
+// ---------------------------------------------------------------------------
+// SDDMM + softmax / LeakyReLU backward in one kernel (one column window,
+// hub-free rows, P2 >= 1): a warp computes dAlpha of its two rows exactly as
+// k_gat_sddmm2 (the whole warp per row), then the softmax backward of each row
+// exactly as k_gat_sbwd4 (16 lanes per row), reading dAlpha back through L2
+// (__ldcg: written by this warp, ordered by __syncwarp) -- bit-identical to the
+// two-kernel path, one launch and one dAlpha round trip to HBM fewer, and the
+// latency-bound row reductions overlap other warps' gathers.
+// ---------------------------------------------------------------------------
+#ifndef GAT_SDSB_MINB
+#define GAT_SDSB_MINB 5  // resident blocks per SM at R <= 2 (4: no spills, measured slower)
+#endif
+template <int H, int R, int P2>
+__global__ void __launch_bounds__(256, R <= 2 ? GAT_SDSB_MINB : (R <= 4 ? 3 : 2))
+    k_gat_sddmm_sbwd(int32_t n, const int32_t* __restrict__ rowptr,
+                     const int32_t* __restrict__ cols, const float4* __restrict__ M,
+                     const float4* __restrict__ G, int32_t k, const float* __restrict__ alpha,
+                     const uint8_t* __restrict__ mask, float beta, float* __restrict__ da,
+                     float* __restrict__ dy, float* __restrict__ dS, SegArgs sg) {
+  static_assert(P2 >= 1, "fused SDDMM: register reductions only");
+  const int32_t w = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  sddmm2_row<H, R, P2, false>(2 * w, 0, n, rowptr, cols, M, G, k, da, sg, nullptr);
+  sddmm2_row<H, R, P2, false>(2 * w + 1, 0, n, rowptr, cols, M, G, k, da, sg, nullptr);
+  __syncwarp();
+  sbwd4_rows<H, true>(2 * w + (lane >= GS ? 1 : 0), n, rowptr, alpha, mask, da, beta, dy, dS,
+                      sg.longest, nullptr);
 }
 
 static inline unsigned sub_grid(int32_t n) { return (unsigned)((n + 256 / GS - 1) / (256 / GS)); }

@@ -146,8 +146,10 @@ np.save(sys.argv[2], np.concatenate([[float(loss)], out.double().cpu().numpy().r
 
 
 def test_fused_attention_aggregation_bit_identical():
-    """The forward's fused attention + aggregation kernel (k_gat_attnagg) gives
-    the same bits as k_gat_attn4 + k_gat_agg2 (SGNN_GAT_FUSE=0, child process)
+    """The forward's fused attention + aggregation kernel (k_gat_attnagg) and
+    the backward's fused SDDMM + softmax backward (k_gat_sddmm_sbwd, register
+    head reductions P2 = 1 and P2 = 2) give the same bits as k_gat_attn4 +
+    k_gat_agg2 / k_gat_sddmm2 + k_gat_sbwd4 (SGNN_GAT_FUSE=0, child process)
     for outputs, cached attention and the backward, on a uniform graph and on a
     power-law graph with hub rows (those keep the segment path)."""
     import os
@@ -160,7 +162,7 @@ import sys, torch, numpy as np
 sys.path.insert(0, '.')
 from paper_2308_12093_b200 import device as d
 res = []
-for kind, h, k in (("er", 8, 32), ("er", 4, 40), ("er", 2, 64), ("pl", 8, 8)):
+for kind, h, k in (("er", 8, 32), ("er", 4, 40), ("er", 2, 64), ("er", 1, 256), ("pl", 8, 8)):
     n = 3000
     s, t = d.synthetic_graph(n, 9.0, 3) if kind == "er" else d.powerlaw_graph(n, 12.0, 2.1, 5)
     P = d.Pattern.gat_pattern(n, s, t)
