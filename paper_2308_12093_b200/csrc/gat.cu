@@ -785,11 +785,12 @@ template <int HH, int RR>
 static void sddmm_sbwd_launch(int mode, cudaStream_t st, int32_t n, const int32_t* rp,
                               const int32_t* ci, const float4* M4, const float4* G4, int32_t k,
                               const float* al, const uint8_t* mk, double beta, float* da,
-                              float* dy, float* dS, const g2::SegArgs& sa) {
+                              float* dy, float* dS, const g2::SegArgs& sa, float* rec,
+                              const int32_t* pinv) {
   const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(n, 16));  // two rows per warp
 #define SDSB_GO(PM) \
   g2::k_gat_sddmm_sbwd<HH, RR, PM><<<grid, 256, 0, st>>>(n, rp, ci, M4, G4, k, al, mk, \
-                                                         (float)beta, da, dy, dS, sa)
+                                                         (float)beta, da, dy, dS, sa, rec, pinv)
   switch (mode) {
     case 1: SDSB_GO(1); return;
     case 2: if constexpr (RR % 2 == 0) { SDSB_GO(2); return; } break;
@@ -799,6 +800,25 @@ static void sddmm_sbwd_launch(int mode, cudaStream_t st, int32_t n, const int32_
   }
 #undef SDSB_GO
   throw invalid_argument("gat: no fused SDDMM kernel for this head width");
+}
+
+// inverse of the pattern's CSC permutation: pinv[perm[p]] = p (CSR edge ->
+// CSC position), built once per pattern on first use (outside graph capture:
+// the first call of a layer runs eagerly, like the LongRows plans)
+__global__ void k_perm_inverse(int64_t q, const int32_t* __restrict__ perm,
+                               int32_t* __restrict__ pinv) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < q;
+       p += (int64_t)gridDim.x * blockDim.x)
+    pinv[__ldg(perm + p)] = (int32_t)p;
+}
+static const int32_t* pattern_pinv(sgnn_ctx ctx, sgnn_pattern P) {
+  if (!P->pinv.get() && P->nnz > 0) {
+    P->pinv = DevBuf((size_t)P->nnz * 4, ctx->stream);
+    k_perm_inverse<<<grid_for(ctx, P->nnz, 256), 256, 0, ctx->stream>>>(
+        P->nnz, P->perm.as<int32_t>(), P->pinv.as<int32_t>());
+    launched(ctx);
+  }
+  return P->pinv.as<int32_t>();
 }
 
 // hub rows / columns of a pattern (LongRows plan): segment arguments
@@ -1368,10 +1388,17 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     // head dots reduce in registers (bit-identical to k_gat_sddmm2 +
     // k_gat_sbwd4; SGNN_GAT_FUSE=0 splits them)
     const bool fuse = wn == 1 && smode >= 1 && gat_fuse_on();
+    // fused path: the softmax backward writes (alpha, dy) records at each
+    // edge's CSC position, so the column pass reads them sequentially
+    // instead of through perm (bit-identical values and order)
+    DevBuf rec;
+    const int32_t* pinv = nullptr;
     if (fuse) {
+      rec = DevBuf((size_t)q * 2 * h * sizeof(float) + 16, st);
+      pinv = pattern_pinv(ctx, p);
       HR_SWITCH(h, R2, (sddmm_sbwd_launch<HH, RR>(smode, st, n, rp, ci, M4, G4, k, al, mk, beta,
                                                   da.as<float>(), dy.as<float>(), dS.as<float>(),
-                                                  sk)));
+                                                  sk, rec.as<float>(), pinv)));
     } else {
       HR_SWITCH(h, R2, (sddmm2_launch<HH, RR, false>(smode, dim3(v2_grid(n), wn), st, n, rp, ci,
                                                      M4, G4, k, da.as<float>(), sk)));
@@ -1389,7 +1416,8 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     if (pr.nlong) {
       HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pr.nlong, 256, 0, st>>>(
                           pr.long_row.as<int32_t>(), rp, al, mk, da.as<float>(), (float)beta,
-                          dy.as<float>(), dS.as<float>())));
+                          dy.as<float>(), dS.as<float>(), nullptr,
+                          fuse ? rec.as<float>() : nullptr, pinv)));
       launched(ctx);
     }
     const int32_t* cpp = p->colptr.as<int32_t>();
@@ -1398,16 +1426,31 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     const float4* as4 = reinterpret_cast<const float4*>(a_src);
     const float4* ad4 = reinterpret_cast<const float4*>(a_dst);
     float4* dM4 = reinterpret_cast<float4*>(dM.get());
-    HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
-                         n, cpp, crw, prm, G4, al, dy.as<float>(), dS.as<float>(), as4, ad4, k,
-                         dD.as<float>(), dM4, skc)));
+    // alpha / dy of the column pass: the interleaved CSC records (fused path)
+    // or the edge-major arrays read through perm
+    const float* cal = fuse ? rec.as<float>() : al;
+    const float* cdy = fuse ? nullptr : dy.as<float>();
+    if (fuse) {
+      HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, false, true><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
+                           n, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
+                           dD.as<float>(), dM4, skc)));
+    } else {
+      HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
+                           n, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
+                           dD.as<float>(), dM4, skc)));
+    }
     launched(ctx);
     if (pc.nlong) {  // hub columns: segment partials + in-order combine
       DevBuf part((size_t)pc.nseg * hk * sizeof(float), st), ddp((size_t)pc.nseg * h * 4, st);
-      HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true><<<dim3(v2_grid(pc.nseg), wn), 256, 0, st>>>(
-                           pc.nseg, cpp, crw, prm, G4, al, dy.as<float>(), dS.as<float>(), as4,
-                           ad4, k, dD.as<float>(), dM4,
-                           seg_args(pc, part.as<float>(), ddp.as<float>()))));
+      if (fuse) {
+        HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true, true><<<dim3(v2_grid(pc.nseg), wn), 256, 0, st>>>(
+                             pc.nseg, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
+                             dD.as<float>(), dM4, seg_args(pc, part.as<float>(), ddp.as<float>()))));
+      } else {
+        HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true><<<dim3(v2_grid(pc.nseg), wn), 256, 0, st>>>(
+                             pc.nseg, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
+                             dD.as<float>(), dM4, seg_args(pc, part.as<float>(), ddp.as<float>()))));
+      }
       launched(ctx);
       HR_SWITCH(h, 1, (g2::k_gat_col_combine<HH><<<v2_grid(pc.nlong), 256, 0, st>>>(
                           pc.nlong, pc.long_row.as<int32_t>(), pc.long_first.as<int32_t>(),

@@ -137,6 +137,19 @@ __device__ __forceinline__ void st_heads(float* __restrict__ p, const float (&v)
   }
 }
 
+// (alpha, dy) edge record, head-interleaved: r[2t] = alpha_t, r[2t+1] = dy_t
+template <int H>
+__device__ __forceinline__ void st_rec(float* __restrict__ r, const float (&a)[H],
+                                       const float (&y)[H]) {
+  if constexpr (H % 2 == 0) {
+#pragma unroll
+    for (int t = 0; t < H; t += 2)
+      reinterpret_cast<float4*>(r)[t / 2] = make_float4(a[t], y[t], a[t + 1], y[t + 1]);
+  } else {
+    *reinterpret_cast<float2*>(r) = make_float2(a[0], y[0]);
+  }
+}
+
 // per-row statistics of the partitioned column pass, [row][head][4] =
 // (s, max, 1 / sum, dot): one 16-byte load per (edge, head) in k_gat_col3
 template <int H>
@@ -745,7 +758,11 @@ __global__ void __launch_bounds__(256, 3)
 // lane (its head), the dX' row R 16-byte vectors; the lanes of a head carry
 // identical dD sums, so no reduction is needed.
 // ---------------------------------------------------------------------------
-template <int H, int R, bool SEG = false>
+// REC: alpha points at (alpha, dy) records in CSC order (st_rec layout, 2H
+// floats per position, written by the softmax backward at the edge's CSC
+// position): one 8-byte load per (edge, head) at p instead of two 4-byte loads
+// through perm (dy unused)
+template <int H, int R, bool SEG = false, bool REC = false>
 __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 : 3)) k_gat_col2(
     int32_t n, const int32_t* __restrict__ colptr, const int32_t* __restrict__ crows,
     const int32_t* __restrict__ perm, const float4* __restrict__ G,
@@ -787,7 +804,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
     float4 x[U][R];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      e[u] = __ldg(perm + p + u);
+      if constexpr (!REC) e[u] = __ldg(perm + p + u);
       row[u] = (uint32_t)__ldg(crows + p + u);
     }
 #pragma unroll
@@ -796,8 +813,14 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
       for (int r = 0; r < R; ++r) {
         const uint32_t v = vo + r * 32 + lane;
         if (r % C == 0) {  // first chunk of its head (every chunk when C == 1)
-          a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
-          dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
+          if constexpr (REC) {
+            const float2 ay = __ldg(reinterpret_cast<const float2*>(alpha) + (int64_t)(p + u) * H + tr[r]);
+            a[u][r] = ay.x;
+            dd[r] += ay.y;
+          } else {
+            a[u][r] = __ldg(alpha + (int64_t)e[u] * H + tr[r]);
+            dd[r] += __ldg(dy + (int64_t)e[u] * H + tr[r]);
+          }
         } else {
           a[u][r] = a[u][r - 1];
         }
@@ -810,13 +833,20 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_MINB : (R >= 8 ? GAT_MINB8 :
         if (vo + r * 32 + lane < fv) fma4(acc[r], a[u][r], x[u][r]);
   }
   for (; p < end; ++p) {
-    const int32_t e = __ldg(perm + p);
+    const int32_t e = REC ? 0 : __ldg(perm + p);
     const uint32_t row = (uint32_t)__ldg(crows + p);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t v = vo + r * 32 + lane;
-      const float a = __ldg(alpha + (int64_t)e * H + tr[r]);
-      dd[r] += __ldg(dy + (int64_t)e * H + tr[r]);
+      float a;
+      if constexpr (REC) {
+        const float2 ay = __ldg(reinterpret_cast<const float2*>(alpha) + (int64_t)p * H + tr[r]);
+        a = ay.x;
+        dd[r] += ay.y;
+      } else {
+        a = __ldg(alpha + (int64_t)e * H + tr[r]);
+        dd[r] += __ldg(dy + (int64_t)e * H + tr[r]);
+      }
       if (v < (uint32_t)fv) fma4(acc[r], a, __ldg(G + row * (uint32_t)fv + v));
     }
   }
@@ -1247,7 +1277,9 @@ __device__ __forceinline__ void sbwd4_rows(int32_t i, int32_t n,
                                            const uint8_t* __restrict__ mask,
                                            const float* __restrict__ da, float beta,
                                            float* __restrict__ dy, float* __restrict__ dS,
-                                           int32_t longest, float* __restrict__ stats) {
+                                           int32_t longest, float* __restrict__ stats,
+                                           float* __restrict__ rec = nullptr,
+                                           const int32_t* __restrict__ pinv = nullptr) {
   const int lane = threadIdx.x & 31, gl = lane & (GS - 1);
   int32_t beg = 0, end = 0;
   if (i < n) {
@@ -1296,7 +1328,11 @@ __device__ __forceinline__ void sbwd4_rows(int32_t i, int32_t n,
         y[t] = (pos >> t) & 1u ? dw : beta * dw;
         rs[t] += y[t];
       }
-      st_heads<H>(dy + (int64_t)e * H, y);
+      if (rec) {  // (alpha, dy) record at the edge's CSC position
+        st_rec<H>(rec + (int64_t)__ldg(pinv + e) * (2 * H), a, y);
+      } else {
+        st_heads<H>(dy + (int64_t)e * H, y);
+      }
     }
   }
   group_allreduce<H>(rs, gl, OpSum());
@@ -1335,7 +1371,8 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_SDSB_MINB : (R <= 4 ? 3 : 2)
                      const int32_t* __restrict__ cols, const float4* __restrict__ M,
                      const float4* __restrict__ G, int32_t k, const float* __restrict__ alpha,
                      const uint8_t* __restrict__ mask, float beta, float* __restrict__ da,
-                     float* __restrict__ dy, float* __restrict__ dS, SegArgs sg) {
+                     float* __restrict__ dy, float* __restrict__ dS, SegArgs sg,
+                     float* __restrict__ rec, const int32_t* __restrict__ pinv) {
   static_assert(P2 >= 1, "fused SDDMM: register reductions only");
   const int32_t w = (int32_t)((blockIdx.x * 256u + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -1343,7 +1380,7 @@ __global__ void __launch_bounds__(256, R <= 2 ? GAT_SDSB_MINB : (R <= 4 ? 3 : 2)
   sddmm2_row<H, R, P2, false>(2 * w + 1, 0, n, rowptr, cols, M, G, k, da, sg, nullptr);
   __syncwarp();
   sbwd4_rows<H, true>(2 * w + (lane >= GS ? 1 : 0), n, rowptr, alpha, mask, da, beta, dy, dS,
-                      sg.longest, nullptr);
+                      sg.longest, nullptr, rec, pinv);
 }
 
 static inline unsigned sub_grid(int32_t n) { return (unsigned)((n + 256 / GS - 1) / (256 / GS)); }
@@ -1464,7 +1501,9 @@ __global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict
                                                        const float* __restrict__ da, float beta,
                                                        float* __restrict__ dy,
                                                        float* __restrict__ dS,
-                                                       float* __restrict__ stats = nullptr) {
+                                                       float* __restrict__ stats = nullptr,
+                                                       float* __restrict__ rec = nullptr,
+                                                       const int32_t* __restrict__ pinv = nullptr) {
   __shared__ float sh[WPB][H];
   const int32_t i = __ldg(long_row + blockIdx.x);
   const int32_t beg = __ldg(rowptr + i), end = __ldg(rowptr + i + 1);
@@ -1491,7 +1530,11 @@ __global__ void __launch_bounds__(256) k_gat_sbwd_long(const int32_t* __restrict
       y[t] = (pos >> t) & 1u ? dw : beta * dw;
       rs[t] += y[t];
     }
-    st_heads<H>(dy + (int64_t)e * H, y);
+    if (rec) {
+      st_rec<H>(rec + (int64_t)__ldg(pinv + e) * (2 * H), a, y);
+    } else {
+      st_heads<H>(dy + (int64_t)e * H, y);
+    }
   }
   block_allreduce<H>(rs, sh, OpSum());
   if (threadIdx.x == 0) st_heads<H>(dS + (int64_t)i * H, rs);

@@ -44,6 +44,7 @@ struct sgnn_pattern_s {
   bool all_self_loops = false;
   sgnn::DevBuf rowptr, cols, colptr, rows, perm, diag;
   sgnn::LongRows long_rows, long_cols;  // hub-row / hub-column plans
+  sgnn::DevBuf pinv;  // CSR edge -> CSC position (lazy; the column pass's edge records)
   ~sgnn_pattern_s();
 };
 
