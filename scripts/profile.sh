@@ -18,7 +18,7 @@ ncu --set full --clock-control none --import-source on -k regex:"k_spmm_lean|k_g
     -s 12 -c 6 -o gpurun_out/full_${TAG} \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-model-cpu --no-large --no-parity > gpurun_out/full_${TAG}.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_gat_attnagg|k_gat_attn4|k_gat_agg2|k_gat_sddmm2|k_gat_sbwd4|k_gat_col2|k_node_scores" \
+    -k regex:"k_gat_attnagg|k_gat_attn4|k_gat_agg2|k_gat_sddmm|k_gat_sbwd4|k_gat_col2|k_node_scores" \
     -s 6 -c 6 -o gpurun_out/full_gat_${TAG} \
     python scripts/kbench.py gat > gpurun_out/full_gat_${TAG}.log 2>&1
 ls -la gpurun_out
