@@ -813,6 +813,11 @@ __global__ void k_perm_inverse(int64_t q, const int32_t* __restrict__ perm,
 }
 static const int32_t* pattern_pinv(sgnn_ctx ctx, sgnn_pattern P) {
   if (!P->pinv.get() && P->nnz > 0) {
+    // not built inside a stream capture (a graph-owned buffer): the caller
+    // then keeps the perm-indirect column pass
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SGNN_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
     P->pinv = DevBuf((size_t)P->nnz * 4, ctx->stream);
     k_perm_inverse<<<grid_for(ctx, P->nnz, 256), 256, 0, ctx->stream>>>(
         P->nnz, P->perm.as<int32_t>(), P->pinv.as<int32_t>());
@@ -1391,11 +1396,10 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     // fused path: the softmax backward writes (alpha, dy) records at each
     // edge's CSC position, so the column pass reads them sequentially
     // instead of through perm (bit-identical values and order)
-    DevBuf rec;
-    const int32_t* pinv = nullptr;
+    const int32_t* pinv = fuse ? pattern_pinv(ctx, p) : nullptr;
+    const bool use_rec = pinv != nullptr;
+    DevBuf rec(use_rec ? (size_t)q * 2 * h * sizeof(float) + 16 : 0, st);
     if (fuse) {
-      rec = DevBuf((size_t)q * 2 * h * sizeof(float) + 16, st);
-      pinv = pattern_pinv(ctx, p);
       HR_SWITCH(h, R2, (sddmm_sbwd_launch<HH, RR>(smode, st, n, rp, ci, M4, G4, k, al, mk, beta,
                                                   da.as<float>(), dy.as<float>(), dS.as<float>(),
                                                   sk, rec.as<float>(), pinv)));
@@ -1417,7 +1421,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
       HR_SWITCH(h, 1, (g2::k_gat_sbwd_long<HH><<<pr.nlong, 256, 0, st>>>(
                           pr.long_row.as<int32_t>(), rp, al, mk, da.as<float>(), (float)beta,
                           dy.as<float>(), dS.as<float>(), nullptr,
-                          fuse ? rec.as<float>() : nullptr, pinv)));
+                          rec.as<float>(), pinv)));
       launched(ctx);
     }
     const int32_t* cpp = p->colptr.as<int32_t>();
@@ -1428,9 +1432,9 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     float4* dM4 = reinterpret_cast<float4*>(dM.get());
     // alpha / dy of the column pass: the interleaved CSC records (fused path)
     // or the edge-major arrays read through perm
-    const float* cal = fuse ? rec.as<float>() : al;
-    const float* cdy = fuse ? nullptr : dy.as<float>();
-    if (fuse) {
+    const float* cal = use_rec ? rec.as<float>() : al;
+    const float* cdy = use_rec ? nullptr : dy.as<float>();
+    if (use_rec) {
       HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, false, true><<<dim3(v2_grid(n), wn), 256, 0, st>>>(
                            n, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
                            dD.as<float>(), dM4, skc)));
@@ -1442,7 +1446,7 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
     launched(ctx);
     if (pc.nlong) {  // hub columns: segment partials + in-order combine
       DevBuf part((size_t)pc.nseg * hk * sizeof(float), st), ddp((size_t)pc.nseg * h * 4, st);
-      if (fuse) {
+      if (use_rec) {
         HR_SWITCH(h, R2, (g2::k_gat_col2<HH, RR, true, true><<<dim3(v2_grid(pc.nseg), wn), 256, 0, st>>>(
                              pc.nseg, cpp, crw, prm, G4, cal, cdy, dS.as<float>(), as4, ad4, k,
                              dD.as<float>(), dM4, seg_args(pc, part.as<float>(), ddp.as<float>()))));
