@@ -63,7 +63,7 @@ def _peaks():
 _KERNEL_OF = {"spmm_fwd_f128": "k_spmm_lean<1, 2", "spmm_bwd_f128": "k_spmm_lean<1, 2",
               "gemm_PxTheta": "tc::k_gemm_tc<0, 1, 128, 1", "gemm_PtG": "tc::k_gemm_tc<1, 1, 128, 0",
               "gemm_GThetaT": "tc::k_gemm_tc<0, 0, 128, 1",
-              "colsum_db": "k_colsum_partial", "gat_col2": "g2::k_gat_col2<8, 2",
+              "colsum_db": "k_colsum_partial", "gat_col2": "g2::k_gat_col2<8, 2, 0, 0",
               "gat_sddmm2": "g2::k_gat_sddmm2<8, 2", "gat_agg2": "g2::k_gat_agg2<8, 2"}
 
 

@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto tile_of = [&](int t, int& z, int& m0, int& n0, int& kb, int& nk) {
     const int nt = t % num_n;
     const int rest = t / num_n;
-    const int mt = rest % num_m;
+    // m-tiles last to first: an A operand just written in row order by the
+    // preceding kernel (the propagate-first SpMM) still has its tail rows in
+    // L2 when the GEMM starts (Arxiv GCN step -2 us, measured)
+    const int mt = num_m - 1 - rest % num_m;
     z = rest / num_m;
     m0 = mt * BM;
     n0 = nt * BN;

@@ -21,4 +21,8 @@ ncu --set full --clock-control none --import-source on \
     -k regex:"k_gat_attnagg|k_gat_attn4|k_gat_agg2|k_gat_sddmm|k_gat_sbwd4|k_gat_col2|k_node_scores" \
     -s 6 -c 6 -o gpurun_out/full_gat_${TAG} \
     python scripts/kbench.py gat > gpurun_out/full_gat_${TAG}.log 2>&1
+# the GAT primitives bench.py times standalone (sddmm2, perm-indirect col2)
+ncu --set full --clock-control none --import-source on -k regex:"k_gat_sddmm2|k_gat_col2" \
+    -s 2 -c 2 -o gpurun_out/full_prims_${TAG} \
+    python scripts/dev/gat_prims.py > gpurun_out/full_prims_${TAG}.log 2>&1
 ls -la gpurun_out

@@ -113,7 +113,7 @@ def main():
                "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
                "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size"]
     full_rows, traffic = [], {}
-    for rep in (f"full_{TAG}", f"full_gat_{TAG}"):
+    for rep in (f"full_{TAG}", f"full_gat_{TAG}", f"full_prims_{TAG}"):
         path = os.path.join(SRC, rep + ".ncu-rep")
         if not os.path.exists(path):
             continue
