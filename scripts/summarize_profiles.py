@@ -71,6 +71,11 @@ def gat2_step(ls):
     """One Gat2 128-(8x256)-(8x40) training step of scripts/dev/gat2_step.py:
     from the layer-1 Theta split + X.Theta GEMM before a node-score launch to
     the same point of the next step (the last complete step)."""
+    # operator-reordered layer 1 (gat_reorder.cuh): the step opens with the
+    # W = Theta a vectors (k_gat_wvec) right before the scores from X
+    idx = [i for i, (n, _) in enumerate(ls) if "k_gat_xscores" in n]
+    if len(idx) >= 2:
+        return ls[idx[-2] - 1:idx[-1] - 1]
     idx = [i for i, (n, _) in enumerate(ls) if "k_node_scores_warp" in n]  # warp or warp4
     if len(idx) < 2:
         return []
