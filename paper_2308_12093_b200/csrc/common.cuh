@@ -69,6 +69,13 @@ struct sgnn_ctx_s {
   // events; captured into CUDA graphs with the main stream)
   cudaStream_t aux = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // tcgen05 GEMM B operand already split into tf32 hi / lo by the caller (on
+  // the side stream, overlapped with earlier work): used by the next GEMM
+  // whose contiguous B is `split_src` with `split_elems` elements
+  const float* split_src = nullptr;
+  int64_t split_elems = 0;
+  const float* split_hi = nullptr;
+  const float* split_lo = nullptr;
 };
 
 namespace sgnn {

@@ -33,6 +33,12 @@ constexpr int dt() {
   return sizeof(T) == 4 ? SGNN_F32 : SGNN_F64;
 }
 
+// SGNN_NO_PRESPLIT=1: split Theta inside the GEMM launch (A/B knob)
+static bool presplit_on() {
+  static const bool on = getenv("SGNN_NO_PRESPLIT") == nullptr;
+  return on;
+}
+
 // out = A' X Theta + b, then (relu != nullptr) ReLU with its mask -- fused into
 // the X.Theta / P.Theta epilogue when that GEMM runs on tcgen05
 template <class T>
@@ -55,8 +61,33 @@ void gcn_forward_t(sgnn_ctx ctx, sgnn_adj A, const T* X, int32_t m, const T* the
   } else {
     DevBuf P((size_t)n * m * sizeof(T), st);
     P.track(kTransient, P.bytes());  // gcn.hpp:114-117
-    spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fwd_plan(ctx, A),
-                A->n_cols);
+    const LongRows* fp = fwd_plan(ctx, A);
+    // float32: Theta's tf32 hi / lo split for the P.Theta GEMM on the side
+    // stream, overlapped with the SpMM (off the step's critical path)
+    DevBuf th_split;
+    bool presplit = false;
+    if constexpr (sizeof(T) == 4)
+      presplit = gemm_uses_presplit((int64_t)m * k, n, m) && presplit_on();
+    if (presplit) {
+      th_split = DevBuf((size_t)m * k * 8, st);
+      SideStream side(ctx);
+      side.side();
+      gemm_presplit_f32(ctx, reinterpret_cast<const float*>(theta), (int64_t)m * k,
+                        th_split.as<float>(), th_split.as<float>() + (size_t)m * k);
+      side.main();
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fp, A->n_cols);
+      side.join();
+      ctx->split_src = reinterpret_cast<const float*>(theta);
+      ctx->split_elems = (int64_t)m * k;
+      ctx->split_hi = th_split.as<float>();
+      ctx->split_lo = th_split.as<float>() + (size_t)m * k;
+    } else {
+      spmm_csr<T>(ctx, n, rp, ci, av, X, m, P.as<T>(), nullptr, A->nnz, fp, A->n_cols);
+    }
+    struct ClearHint {  // the hint covers this GEMM only (also on exceptions)
+      sgnn_ctx c;
+      ~ClearHint() { c->split_src = nullptr; c->split_elems = 0; }
+    } clear_hint{ctx};
     bool fused = false;
     if constexpr (sizeof(T) == 4)
       if (relu) fused = gemm_relu_f32(ctx, P.as<T>(), n, m, theta, m, k, false, false, out, bias,

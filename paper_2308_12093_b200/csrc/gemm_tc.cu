@@ -1202,6 +1202,14 @@ bool gemm_tc_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const flo
                  float* d_out, int heads, uint8_t* relu_out, const uint8_t* mask_in,
                  const float* elu_saved);
 
+void gemm_presplit_f32(sgnn_ctx ctx, const float* B, int64_t elems, float* hi, float* lo) {
+  tc::k_split_global<<<grid_for(ctx, elems, 256), 256, 0, ctx->stream>>>(elems, B, hi, lo);
+  launched(ctx);
+}
+bool gemm_uses_presplit(int64_t elems, int32_t ra, int32_t ca) {
+  return elems * 8 <= (int64_t)ra * ca;  // = `pre` in the launcher below
+}
+
 // Operands with stored widths that are not multiples of 4: stage padded
 // copies (K padded with zeros on both operands, M / N padded as stored
 // widths), run the tcgen05 GEMM on them and copy the M x N block back.
@@ -1364,7 +1372,12 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
   const bool okA = a_mn ? make_map(&mp.a, A, M, K, lda, BK, true)
                         : make_map(&mp.a, A, K, M, lda, BM, false);
   if (!okA) return false;
-  if (pre) {
+  // the caller split B already (gemm_presplit_f32 on its side stream)
+  const bool hinted = pre && ldb == cb && ctx->split_src == B && ctx->split_elems == belems;
+  if (hinted) {
+    Bhi = ctx->split_hi;
+    Blo = ctx->split_lo;
+  } else if (pre) {
     bsplit = DevBuf((size_t)belems * 8, ctx->stream);
     Bhi = bsplit.as<float>();
     Blo = bsplit.as<float>() + belems;
@@ -1425,7 +1438,7 @@ static bool gemm_tc_f32_impl(sgnn_ctx ctx, const float* A, int32_t ra, int32_t c
         (reinterpret_cast<uintptr_t>(mask_in) & 15))
       return false;
   }
-  if (pre) {
+  if (pre && !hinted) {
     if (ldb == cb)
       k_split_global<<<grid_for(ctx, belems, 256), 256, 0, ctx->stream>>>(
           belems, B, bsplit.as<float>(), bsplit.as<float>() + belems);

@@ -99,6 +99,11 @@ bool gemm_scores_f32(sgnn_ctx ctx, const float* X, int32_t n, int32_t m, const f
                      int32_t hk, float* M, const float* a_src, const float* a_dst, int32_t h,
                      float* s, float* d);
 
+// split a contiguous fp32 matrix into tf32 hi / lo (the tcgen05 GEMM's
+// pre-split B) on ctx->stream; true if the GEMM of an ra x ca A would use a
+// pre-split B of `elems` elements
+void gemm_presplit_f32(sgnn_ctx ctx, const float* B, int64_t elems, float* hi, float* lo);
+bool gemm_uses_presplit(int64_t elems, int32_t ra, int32_t ca);
 bool gemm_relu_f32(sgnn_ctx ctx, const float* A, int32_t ra, int32_t ca, const float* B,
                    int32_t rb, int32_t cb, bool ta, bool tb, float* C, const float* bias,
                    uint8_t* relu_out, const uint8_t* mask_in);
