@@ -750,6 +750,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       float ss = 0.f, sd = 0.f;  // fused node scores of the current head
       int hrem = sc.k >> 2, head = (EPI & 8) ? n0 / sc.k : 0;
+      // k = 32 with 4 heads per 128-wide tile (h % 4 == 0): a row's four
+      // head scores leave as one 16-byte store per array at the tile's end
+      const bool vsc = (EPI & 1) && !(EPI & 8) && BN == 128 && sc.k == 32 &&
+                       (sc.h & 3) == 0 && (N & 127) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(sc.s) | reinterpret_cast<uintptr_t>(sc.d)) & 15) == 0;
+      float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f), d4 = s4;
       // software pipeline over the 32-column chunks: the TMEM load of chunk
       // c + 32 (and lane j's bias of its column j) is in flight while chunk c
       // is processed, and the accumulator goes back to the MMA warp as soon as
@@ -808,7 +814,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ss = fmaf(m3, as.w, fmaf(m2, as.z, fmaf(m1, as.y, fmaf(m0, as.x, ss))));
               sd = fmaf(m3, ad.w, fmaf(m2, ad.z, fmaf(m1, ad.y, fmaf(m0, ad.x, sd))));
             }
-            if ((col0 + 32) % sc.k == 0) {
+            if (vsc) {  // shift the head's scores in; store after the 4th head
+              s4 = make_float4(s4.y, s4.z, s4.w, ss);
+              d4 = make_float4(d4.y, d4.z, d4.w, sd);
+              if (c + 32 == BN && row < M) {
+                *reinterpret_cast<float4*>(sc.s + (int64_t)row * sc.h + n0 / 32) = s4;
+                *reinterpret_cast<float4*>(sc.d + (int64_t)row * sc.h + n0 / 32) = d4;
+              }
+              ss = sd = 0.f;
+            } else if ((col0 + 32) % sc.k == 0) {
               if (row < M) {
                 sc.s[(int64_t)row * sc.h + col0 / sc.k] = ss;
                 sc.d[(int64_t)row * sc.h + col0 / sc.k] = sd;
