@@ -1462,6 +1462,13 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
                           dD.as<float>(), dM4)));
       launched(ctx);
     }
+    // dTheta = X^T dM on the side stream, overlapped with the attention
+    // gradients and dX = dM Theta^T here (independent consumers of dM)
+    SideStream side(ctx);
+    side.side();
+    gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
+            d_theta);
+    side.main();
     {  // d_bias, d_a_src, d_a_dst: one pass over dX' and M
       const int32_t nb = std::max<int32_t>(1, std::min<int32_t>(4 * ctx->num_sms, n));
       const int32_t chunk = (int32_t)ceil_div(n, nb);
@@ -1478,9 +1485,8 @@ void gat_backward_t(sgnn_ctx ctx, sgnn_pattern p, const T* G, const T* theta, co
           reinterpret_cast<float*>(d_a_src), reinterpret_cast<float*>(d_a_dst));
       launched(ctx);
     }
-    gemm<T>(ctx, static_cast<const T*>(c->saved_input), n, m, dM.as<T>(), n, hk, true, false,
-            d_theta);
     if (fg) dx_gemm(dM.as<T>());
+    side.join();
     return;
   }
   {
