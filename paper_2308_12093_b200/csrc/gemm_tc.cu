@@ -382,7 +382,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // m-tiles last to first: an A operand just written in row order by the
     // preceding kernel (the propagate-first SpMM) still has its tail rows in
     // L2 when the GEMM starts (Arxiv GCN step -2 us, measured)
+#ifndef GEMM_FWD_M
     const int mt = num_m - 1 - rest % num_m;
+#else
+    const int mt = rest % num_m;
+#endif
     z = rest / num_m;
     m0 = mt * BM;
     n0 = nt * BN;
